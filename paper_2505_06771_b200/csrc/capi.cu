@@ -1,0 +1,760 @@
+// capi.cu — the C ABI of include/mrsim_cuda.h: context lifetime, batch
+// state in HBM (two ping-pong SoA copies), kernel dispatch per
+// (task, group width, precision), host-buffer step, state/stats I/O and
+// device error reporting. No CPU fallback exists: every compute entry point
+// launches the sm_100a kernels or fails with MRSIM_E_CUDA.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "launch.h"
+#include "mrsim_cuda.h"
+
+using mrsim_dev::DevState;
+using mrsim_dev::EnvStats;
+using mrsim_dev::ResetParams;
+using mrsim_dev::StepParams;
+
+struct mrsim_ctx {
+    mrsim_cfg cfg;
+    int device = 0;
+    long long B = 0;
+    unsigned flags = 0;
+    bool fp64 = false;
+    int N = 0, n = 0, P = 0, D = 0, bdim = 0, nf = 0, ni = 0, L = 8;
+    void* mem[2] = {nullptr, nullptr};
+    DevState<float> sf[2];
+    DevState<double> sd[2];
+    void* stats_mem = nullptr;
+    EnvStats st{};
+    unsigned long long* d_err = nullptr;
+    long long* d_err_serial = nullptr;
+    int cur = 0;
+    long long serial = 0;
+    int hist_in[64] = {0};
+    bool has_episodes = false;
+    uint64_t root_seed = 0;
+    long long episode_stride = 0;
+    long long env_steps = 0;
+    std::string last_error;
+    int num_sms = 148;
+    int block = 256;
+    int grid = 0;
+    int smem_group = 0;
+    // host-API scratch
+    int8_t* d_actions = nullptr;
+    float* d_obs = nullptr;
+    float* d_reward = nullptr;
+    uint8_t* d_done = nullptr;
+    int8_t* h_actions = nullptr;  // pinned
+    bool reset_done = false;
+};
+
+namespace {
+
+int set_err(mrsim_ctx* ctx, int code, const std::string& msg) {
+    if (ctx) ctx->last_error = msg;
+    return code;
+}
+
+int cuda_fail(mrsim_ctx* ctx, cudaError_t e, const char* where) {
+    return set_err(ctx, MRSIM_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(expr)                                                    \
+    do {                                                            \
+        cudaError_t _e = (expr);                                    \
+        if (_e != cudaSuccess) return cuda_fail(ctx, _e, #expr);    \
+    } while (0)
+
+template <class Real>
+size_t state_bytes(long long B, int N, int nf, int ni) {
+    size_t b = 0;
+    auto add = [&](size_t bytes) { b += (bytes + 255) & ~size_t(255); };
+    for (int k = 0; k < 3; ++k) add(sizeof(Real) * B * N);
+    add(4 * B);                      // step_index
+    for (int k = 0; k < 3; ++k) add(8 * B);  // key, seed, pkey
+    add(8 * B);                      // episode
+    for (int k = 0; k < 3; ++k) add(4 * B);  // collisions, qp_inf, success
+    for (int k = 0; k < 3; ++k) add(sizeof(Real) * B);  // metric, min_dist, ep_return
+    add(sizeof(Real) * B * (nf > 0 ? nf : 1));
+    add(4 * B * (ni > 0 ? ni : 1));
+    return b;
+}
+
+template <class Real>
+void carve_state(void* base, long long B, int N, int nf, int ni, DevState<Real>& s) {
+    char* p = static_cast<char*>(base);
+    auto take = [&](size_t bytes) {
+        char* r = p;
+        p += (bytes + 255) & ~size_t(255);
+        return r;
+    };
+    s.px = reinterpret_cast<Real*>(take(sizeof(Real) * B * N));
+    s.py = reinterpret_cast<Real*>(take(sizeof(Real) * B * N));
+    s.pt = reinterpret_cast<Real*>(take(sizeof(Real) * B * N));
+    s.step_index = reinterpret_cast<int32_t*>(take(4 * B));
+    s.key = reinterpret_cast<uint64_t*>(take(8 * B));
+    s.seed = reinterpret_cast<uint64_t*>(take(8 * B));
+    s.pkey = reinterpret_cast<uint64_t*>(take(8 * B));
+    s.episode = reinterpret_cast<int64_t*>(take(8 * B));
+    s.collisions = reinterpret_cast<int32_t*>(take(4 * B));
+    s.qp_inf = reinterpret_cast<int32_t*>(take(4 * B));
+    s.success = reinterpret_cast<int32_t*>(take(4 * B));
+    s.metric = reinterpret_cast<Real*>(take(sizeof(Real) * B));
+    s.min_dist = reinterpret_cast<Real*>(take(sizeof(Real) * B));
+    s.ep_return = reinterpret_cast<Real*>(take(sizeof(Real) * B));
+    s.tf = reinterpret_cast<Real*>(take(sizeof(Real) * B * (nf > 0 ? nf : 1)));
+    s.ti = reinterpret_cast<int32_t*>(take(4 * B * (ni > 0 ? ni : 1)));
+}
+
+// ---- dispatch tables over the task template parameter ----
+template <class Real>
+cudaError_t dispatch_step(int task, const StepParams<Real>& p, int L, int grid, int block, int smem,
+                          cudaStream_t s) {
+    using namespace mrsim_host;
+    switch (task) {
+        case 0: return launch_step<Real, 0>(p, L, grid, block, smem, s);
+        case 1: return launch_step<Real, 1>(p, L, grid, block, smem, s);
+        case 2: return launch_step<Real, 2>(p, L, grid, block, smem, s);
+        case 3: return launch_step<Real, 3>(p, L, grid, block, smem, s);
+        case 4: return launch_step<Real, 4>(p, L, grid, block, smem, s);
+        case 5: return launch_step<Real, 5>(p, L, grid, block, smem, s);
+        case 6: return launch_step<Real, 6>(p, L, grid, block, smem, s);
+        default: return launch_step<Real, 7>(p, L, grid, block, smem, s);
+    }
+}
+template <class Real>
+cudaError_t dispatch_occ(int task, int L, int block, int smem, int* bps) {
+    using namespace mrsim_host;
+    switch (task) {
+        case 0: return step_occupancy<Real, 0>(L, block, smem, bps);
+        case 1: return step_occupancy<Real, 1>(L, block, smem, bps);
+        case 2: return step_occupancy<Real, 2>(L, block, smem, bps);
+        case 3: return step_occupancy<Real, 3>(L, block, smem, bps);
+        case 4: return step_occupancy<Real, 4>(L, block, smem, bps);
+        case 5: return step_occupancy<Real, 5>(L, block, smem, bps);
+        case 6: return step_occupancy<Real, 6>(L, block, smem, bps);
+        default: return step_occupancy<Real, 7>(L, block, smem, bps);
+    }
+}
+template <class Real>
+cudaError_t dispatch_reset(int task, const ResetParams<Real>& p, cudaStream_t s) {
+    using namespace mrsim_host;
+    switch (task) {
+        case 0: return launch_reset<Real, 0>(p, s);
+        case 1: return launch_reset<Real, 1>(p, s);
+        case 2: return launch_reset<Real, 2>(p, s);
+        case 3: return launch_reset<Real, 3>(p, s);
+        case 4: return launch_reset<Real, 4>(p, s);
+        case 5: return launch_reset<Real, 5>(p, s);
+        case 6: return launch_reset<Real, 6>(p, s);
+        default: return launch_reset<Real, 7>(p, s);
+    }
+}
+
+const char* err_text(unsigned code) {
+    switch (code) {
+        case mrsim_dev::kErrInvalidAction: return "step_batch: invalid action";
+        case mrsim_dev::kErrCoincident: return "build_barrier_constraints: coincident robot positions";
+        case mrsim_dev::kErrNonFinite: return "wrap_angle: non-finite input";
+        case mrsim_dev::kErrSpawn: return "sample_poses: could not place robot";
+        case mrsim_dev::kErrGoals: return "navigation: could not place goals";
+        case mrsim_dev::kErrPrey: return "predator_prey: could not place prey";
+        default: return "unknown device error";
+    }
+}
+int err_code(unsigned code) {
+    switch (code) {
+        case mrsim_dev::kErrInvalidAction: return MRSIM_E_INVALID_ARGUMENT;
+        case mrsim_dev::kErrCoincident:
+        case mrsim_dev::kErrNonFinite: return MRSIM_E_DOMAIN;
+        default: return MRSIM_E_RUNTIME;
+    }
+}
+
+// Read the sticky device error word; returns MRSIM_OK or the mapped code.
+int check_device_error(mrsim_ctx* ctx, bool rollback) {
+    unsigned long long w = 0;
+    long long ser = -1;
+    cudaError_t e = cudaMemcpy(&w, ctx->d_err, sizeof w, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "read device error");
+    if (w == ~0ull) return MRSIM_OK;
+    cudaMemcpy(&ser, ctx->d_err_serial, sizeof ser, cudaMemcpyDeviceToHost);
+    const unsigned code = static_cast<unsigned>(w & 0xff);
+    const int detail = static_cast<int>((w >> 8) & 0xff);
+    const int robot = static_cast<int>((w >> 16) & 0xff);
+    const long long env = static_cast<long long>(w >> 24);
+    char buf[256];
+    if (code == mrsim_dev::kErrInvalidAction)
+        std::snprintf(buf, sizeof buf, "step_batch: invalid action %d for environment %lld, robot %d",
+                      static_cast<int8_t>(detail), env, robot);
+    else if (code == mrsim_dev::kErrSpawn)
+        std::snprintf(buf, sizeof buf, "sample_poses: could not place robot %d after 1000 attempts (environment %lld)",
+                      robot, env);
+    else
+        std::snprintf(buf, sizeof buf, "%s (environment %lld, robot %d)", err_text(code), env, robot);
+    if (rollback && ser >= 0 && ser < ctx->serial && ctx->serial - ser <= 64) {
+        ctx->cur = ctx->hist_in[ser % 64];  // state as it was before the failing step
+    }
+    // clear so the context stays usable after the caller handled the error
+    const unsigned long long none = ~0ull;
+    cudaMemcpy(ctx->d_err, &none, sizeof none, cudaMemcpyHostToDevice);
+    return set_err(ctx, err_code(code), buf);
+}
+
+template <class Real>
+int do_step(mrsim_ctx* ctx, DevState<Real>* s, const int8_t* actions, float* obs, float* reward, uint8_t* done,
+            float* next_obs, cudaStream_t stream) {
+    StepParams<Real> p;
+    std::memset(&p, 0, sizeof p);
+    p.c = ctx->cfg;
+    p.in = s[ctx->cur];
+    p.out = s[1 - ctx->cur];
+    p.st = ctx->st;
+    p.actions = actions;
+    p.obs = obs;
+    p.reward = reward;
+    p.done = done;
+    p.next_obs = next_obs;
+    p.err = ctx->d_err;
+    p.err_serial = ctx->d_err_serial;
+    p.serial = ctx->serial;
+    p.B = ctx->B;
+    p.N = ctx->N;
+    p.n = ctx->n;
+    p.P = ctx->P;
+    p.D = ctx->D;
+    p.bdim = ctx->bdim;
+    p.nf = ctx->nf;
+    p.ni = ctx->ni;
+    p.auto_reset = (ctx->flags & MRSIM_FLAG_AUTO_RESET) ? 1 : 0;
+    p.root_seed = ctx->root_seed;
+    p.episode_stride = ctx->episode_stride;
+    p.smem_bytes_per_group = ctx->smem_group;
+    mrsim_host::fill_consts(ctx->cfg, p.k);
+    const int smem = ctx->smem_group * (ctx->block / ctx->L);
+    cudaError_t e = dispatch_step<Real>(ctx->cfg.task, p, ctx->L, ctx->grid, ctx->block, smem, stream);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "step kernel launch");
+    ctx->hist_in[ctx->serial % 64] = ctx->cur;
+    ctx->serial += 1;
+    ctx->cur = 1 - ctx->cur;
+    ctx->env_steps += ctx->B;
+    return MRSIM_OK;
+}
+
+template <class Real>
+int do_reset(mrsim_ctx* ctx, DevState<Real>* s, const uint64_t* d_seeds, uint64_t root, long long first,
+             float* obs, cudaStream_t stream) {
+    ResetParams<Real> p;
+    std::memset(&p, 0, sizeof p);
+    p.c = ctx->cfg;
+    p.out = s[ctx->cur];
+    p.seeds = d_seeds;
+    p.root_seed = root;
+    p.first_episode = first;
+    p.obs = obs;
+    p.err = ctx->d_err;
+    p.B = ctx->B;
+    p.N = ctx->N;
+    p.D = ctx->D;
+    p.bdim = ctx->bdim;
+    p.nf = ctx->nf;
+    p.ni = ctx->ni;
+    cudaError_t e = dispatch_reset<Real>(ctx->cfg.task, p, stream);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "reset kernel launch");
+    return MRSIM_OK;
+}
+
+template <class Real>
+void to_host_states(mrsim_ctx* ctx, const DevState<Real>& s, long long first, long long count,
+                    mrsim_env_state* out, cudaError_t* err) {
+    const int N = ctx->N;
+    std::vector<Real> px(count * N), py(count * N), pt(count * N), metric(count), mind(count), ret(count);
+    std::vector<int32_t> step(count), coll(count), qpi(count), succ(count);
+    std::vector<uint64_t> key(count), seed(count);
+    std::vector<int64_t> ep(count);
+    std::vector<Real> tf(static_cast<size_t>(count) * (ctx->nf > 0 ? ctx->nf : 1));
+    std::vector<int32_t> ti(static_cast<size_t>(count) * (ctx->ni > 0 ? ctx->ni : 1));
+    cudaError_t e = cudaSuccess;
+    auto cp = [&](void* dst, const void* src, size_t bytes) {
+        if (e == cudaSuccess) e = cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost);
+    };
+    cp(px.data(), s.px + first * N, sizeof(Real) * count * N);
+    cp(py.data(), s.py + first * N, sizeof(Real) * count * N);
+    cp(pt.data(), s.pt + first * N, sizeof(Real) * count * N);
+    cp(step.data(), s.step_index + first, 4 * count);
+    cp(key.data(), s.key + first, 8 * count);
+    cp(seed.data(), s.seed + first, 8 * count);
+    cp(ep.data(), s.episode + first, 8 * count);
+    cp(coll.data(), s.collisions + first, 4 * count);
+    cp(qpi.data(), s.qp_inf + first, 4 * count);
+    cp(succ.data(), s.success + first, 4 * count);
+    cp(metric.data(), s.metric + first, sizeof(Real) * count);
+    cp(mind.data(), s.min_dist + first, sizeof(Real) * count);
+    cp(ret.data(), s.ep_return + first, sizeof(Real) * count);
+    for (int f = 0; f < ctx->nf; ++f) cp(tf.data() + f * count, s.tf + f * ctx->B + first, sizeof(Real) * count);
+    for (int w = 0; w < ctx->ni; ++w) cp(ti.data() + w * count, s.ti + w * ctx->B + first, 4 * count);
+    *err = e;
+    if (e != cudaSuccess) return;
+    const mrsim_cfg& c = ctx->cfg;
+    const mrsim_layout& y = c.layout;
+    for (long long k = 0; k < count; ++k) {
+        mrsim_env_state& o = out[k];
+        std::memset(&o, 0, sizeof o);
+        o.num_robots = N;
+        o.step_index = step[k];
+        o.rng_key = key[k];
+        o.seed = seed[k];
+        o.episode = ep[k];
+        for (int i = 0; i < N; ++i) {
+            o.x[i] = double(px[k * N + i]);
+            o.y[i] = double(py[k * N + i]);
+            o.theta[i] = double(pt[k * N + i]);
+        }
+        o.collisions = coll[k];
+        o.qp_infeasible = qpi[k];
+        o.success = succ[k];
+        o.scenario_metric = double(metric[k]);
+        o.min_pairwise_distance = double(mind[k]);
+        o.episode_return = double(ret[k]);
+        auto TF = [&](int f) { return double(tf[static_cast<size_t>(f) * count + k]); };
+        auto TI = [&](int w) { return ti[static_cast<size_t>(w) * count + k]; };
+        auto TB = [&](int b) { return (TI(b >> 2) >> (8 * (b & 3))) & 0xff; };
+        switch (c.task) {
+            case MRSIM_TASK_NAVIGATION:
+                for (int i = 0; i < N; ++i) { o.goals[i][0] = TF(2 * i); o.goals[i][1] = TF(2 * i + 1); }
+                break;
+            case MRSIM_TASK_PREDATOR_PREY:
+                o.prey[0] = TF(0); o.prey[1] = TF(1); o.flash_timer = TI(0);
+                break;
+            case MRSIM_TASK_DISCOVERY:
+                o.num_landmarks = y.discovery_num_landmarks;
+                for (int q = 0; q < o.num_landmarks; ++q) {
+                    o.landmarks[q][0] = TF(2 * q);
+                    o.landmarks[q][1] = TF(2 * q + 1);
+                    o.sensed[q] = (TI(0) >> q) & 1;
+                    o.tagged[q] = (TI(1) >> q) & 1;
+                }
+                break;
+            case MRSIM_TASK_RWARE: {
+                const int S = y.rware_num_slots, R = mrsim_dev::rware_requests(y);
+                o.num_slots = S;
+                o.num_requests = R;
+                for (int q = 0; q < S; ++q) o.slot_shelf[q] = TB(q);
+                for (int i = 0; i < N; ++i) o.carried[i] = TB(S + i);
+                for (int q = 0; q < R; ++q) o.requests[q] = TB(S + N + q);
+                break;
+            }
+            case MRSIM_TASK_FORAGING:
+                o.num_resources = y.foraging_num_resources;
+                for (int q = 0; q < o.num_resources; ++q) {
+                    o.resources[q][0] = TF(2 * q);
+                    o.resources[q][1] = TF(2 * q + 1);
+                    o.levels[q] = TI(1 + q);
+                    o.foraged[q] = (TI(0) >> q) & 1;
+                }
+                break;
+            case MRSIM_TASK_MATERIAL_TRANSPORT:
+                o.circle_remaining = TF(0); o.rect_remaining = TF(1); o.delivered = TF(2); o.total_initial = TF(3);
+                for (int i = 0; i < N; ++i) o.loads[i] = TF(4 + i);
+                break;
+            case MRSIM_TASK_ARCTIC_TRANSPORT:
+                o.cols = y.arctic_grid_cols;
+                o.rows = y.arctic_grid_rows;
+                std::memcpy(o.goal_zone, y.arctic_goal_zone, sizeof o.goal_zone);
+                for (int t = 0; t < o.cols * o.rows; ++t) o.tiles[t] = static_cast<int8_t>(TB(t));
+                break;
+            case MRSIM_TASK_WAREHOUSE:
+                for (int i = 0; i < N; ++i) o.loaded[i] = (TI(0) >> i) & 1;
+                break;
+        }
+    }
+}
+
+template <class Real>
+void from_host_states(mrsim_ctx* ctx, const DevState<Real>& s, long long first, long long count,
+                      const mrsim_env_state* in, cudaError_t* err) {
+    const int N = ctx->N;
+    const mrsim_cfg& c = ctx->cfg;
+    const mrsim_layout& y = c.layout;
+    std::vector<Real> px(count * N), py(count * N), pt(count * N), metric(count), mind(count), ret(count);
+    std::vector<int32_t> step(count), coll(count), qpi(count), succ(count);
+    std::vector<uint64_t> key(count), seed(count), pkey(count);
+    std::vector<int64_t> ep(count);
+    std::vector<Real> tf(static_cast<size_t>(count) * (ctx->nf > 0 ? ctx->nf : 1), Real(0));
+    std::vector<int32_t> ti(static_cast<size_t>(count) * (ctx->ni > 0 ? ctx->ni : 1), 0);
+    for (long long k = 0; k < count; ++k) {
+        const mrsim_env_state& o = in[k];
+        for (int i = 0; i < N; ++i) {
+            px[k * N + i] = Real(o.x[i]);
+            py[k * N + i] = Real(o.y[i]);
+            pt[k * N + i] = Real(o.theta[i]);
+        }
+        step[k] = o.step_index;
+        key[k] = o.rng_key;
+        seed[k] = o.seed;
+        pkey[k] = mrsim_dev::policy_key_of(o.seed);
+        ep[k] = o.episode;
+        coll[k] = static_cast<int32_t>(o.collisions);
+        qpi[k] = static_cast<int32_t>(o.qp_infeasible);
+        succ[k] = o.success;
+        metric[k] = Real(o.scenario_metric);
+        mind[k] = Real(o.min_pairwise_distance);
+        ret[k] = Real(o.episode_return);
+        auto TF = [&](int f, double v) { tf[static_cast<size_t>(f) * count + k] = Real(v); };
+        auto TI = [&](int w, int v) { ti[static_cast<size_t>(w) * count + k] = v; };
+        auto TB = [&](int b, int v) {
+            int32_t& w = ti[static_cast<size_t>(b >> 2) * count + k];
+            const int sh = 8 * (b & 3);
+            w = (w & ~(0xff << sh)) | ((v & 0xff) << sh);
+        };
+        switch (c.task) {
+            case MRSIM_TASK_NAVIGATION:
+                for (int i = 0; i < N; ++i) { TF(2 * i, o.goals[i][0]); TF(2 * i + 1, o.goals[i][1]); }
+                break;
+            case MRSIM_TASK_PREDATOR_PREY:
+                TF(0, o.prey[0]); TF(1, o.prey[1]); TI(0, o.flash_timer);
+                break;
+            case MRSIM_TASK_DISCOVERY: {
+                int sm = 0, tg = 0;
+                for (int q = 0; q < y.discovery_num_landmarks; ++q) {
+                    TF(2 * q, o.landmarks[q][0]);
+                    TF(2 * q + 1, o.landmarks[q][1]);
+                    sm |= (o.sensed[q] ? 1 : 0) << q;
+                    tg |= (o.tagged[q] ? 1 : 0) << q;
+                }
+                TI(0, sm);
+                TI(1, tg);
+                break;
+            }
+            case MRSIM_TASK_RWARE: {
+                const int S = y.rware_num_slots, R = mrsim_dev::rware_requests(y);
+                for (int q = 0; q < S; ++q) TB(q, o.slot_shelf[q]);
+                for (int i = 0; i < N; ++i) TB(S + i, o.carried[i]);
+                for (int q = 0; q < R; ++q) TB(S + N + q, o.requests[q]);
+                break;
+            }
+            case MRSIM_TASK_FORAGING: {
+                int fm = 0;
+                for (int q = 0; q < y.foraging_num_resources; ++q) {
+                    TF(2 * q, o.resources[q][0]);
+                    TF(2 * q + 1, o.resources[q][1]);
+                    TI(1 + q, o.levels[q]);
+                    fm |= (o.foraged[q] ? 1 : 0) << q;
+                }
+                TI(0, fm);
+                break;
+            }
+            case MRSIM_TASK_MATERIAL_TRANSPORT:
+                TF(0, o.circle_remaining); TF(1, o.rect_remaining); TF(2, o.delivered); TF(3, o.total_initial);
+                for (int i = 0; i < N; ++i) TF(4 + i, o.loads[i]);
+                break;
+            case MRSIM_TASK_ARCTIC_TRANSPORT:
+                for (int t = 0; t < y.arctic_grid_cols * y.arctic_grid_rows; ++t) TB(t, o.tiles[t]);
+                break;
+            case MRSIM_TASK_WAREHOUSE: {
+                int lm = 0;
+                for (int i = 0; i < N; ++i) lm |= (o.loaded[i] ? 1 : 0) << i;
+                TI(0, lm);
+                break;
+            }
+        }
+    }
+    cudaError_t e = cudaSuccess;
+    auto cp = [&](void* dst, const void* src, size_t bytes) {
+        if (e == cudaSuccess) e = cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice);
+    };
+    cp(s.px + first * N, px.data(), sizeof(Real) * count * N);
+    cp(s.py + first * N, py.data(), sizeof(Real) * count * N);
+    cp(s.pt + first * N, pt.data(), sizeof(Real) * count * N);
+    cp(s.step_index + first, step.data(), 4 * count);
+    cp(s.key + first, key.data(), 8 * count);
+    cp(s.seed + first, seed.data(), 8 * count);
+    cp(s.pkey + first, pkey.data(), 8 * count);
+    cp(s.episode + first, ep.data(), 8 * count);
+    cp(s.collisions + first, coll.data(), 4 * count);
+    cp(s.qp_inf + first, qpi.data(), 4 * count);
+    cp(s.success + first, succ.data(), 4 * count);
+    cp(s.metric + first, metric.data(), sizeof(Real) * count);
+    cp(s.min_dist + first, mind.data(), sizeof(Real) * count);
+    cp(s.ep_return + first, ret.data(), sizeof(Real) * count);
+    for (int f = 0; f < ctx->nf; ++f) cp(s.tf + f * ctx->B + first, tf.data() + f * count, sizeof(Real) * count);
+    for (int w = 0; w < ctx->ni; ++w) cp(s.ti + w * ctx->B + first, ti.data() + w * count, 4 * count);
+    *err = e;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mrsim_create(const mrsim_cfg* cfg, int device, int64_t num_envs, uint32_t flags, mrsim_ctx** out) {
+    if (!cfg || !out || num_envs < 1) return MRSIM_E_INVALID_ARGUMENT;
+    *out = nullptr;
+    char msg[256] = {0};
+    int rc = mrsim_config_validate(cfg, msg, sizeof msg);
+    if (rc != MRSIM_OK) {
+        std::fprintf(stderr, "mrsim_create: %s\n", msg);
+        return rc;
+    }
+    mrsim_ctx* ctx = new mrsim_ctx;
+    ctx->cfg = *cfg;
+    ctx->device = device;
+    ctx->B = num_envs;
+    ctx->flags = flags;
+    ctx->fp64 = (flags & MRSIM_FLAG_FP64) != 0;
+    ctx->N = cfg->num_robots;
+    ctx->n = 2 * ctx->N;
+    ctx->P = ctx->N * (ctx->N - 1) / 2;
+    ctx->D = mrsim_dev::obs_dim_of(*cfg);
+    ctx->bdim = mrsim_dev::base_obs_dim(*cfg);
+    mrsim_dev::task_fields(*cfg, &ctx->nf, &ctx->ni);
+    ctx->L = ctx->n <= 8 ? 8 : (ctx->n <= 16 ? 16 : 32);
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) {
+        rc = cuda_fail(ctx, e, "cudaSetDevice");
+        std::fprintf(stderr, "mrsim_create: %s\n", ctx->last_error.c_str());
+        delete ctx;
+        return rc;
+    }
+    auto bail = [&](cudaError_t err, const char* where) {
+        int code = cuda_fail(ctx, err, where);
+        std::fprintf(stderr, "mrsim_create: %s\n", ctx->last_error.c_str());
+        mrsim_destroy(ctx);
+        return code;
+    };
+    cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+    const size_t sb = ctx->fp64 ? state_bytes<double>(ctx->B, ctx->N, ctx->nf, ctx->ni)
+                                : state_bytes<float>(ctx->B, ctx->N, ctx->nf, ctx->ni);
+    for (int k = 0; k < 2; ++k) {
+        if ((e = cudaMalloc(&ctx->mem[k], sb)) != cudaSuccess) return bail(e, "cudaMalloc state");
+        cudaMemset(ctx->mem[k], 0, sb);
+        if (ctx->fp64) carve_state(ctx->mem[k], ctx->B, ctx->N, ctx->nf, ctx->ni, ctx->sd[k]);
+        else carve_state(ctx->mem[k], ctx->B, ctx->N, ctx->nf, ctx->ni, ctx->sf[k]);
+    }
+    const size_t stb = static_cast<size_t>(ctx->B) * (4 + 8 * 5 + 8 * 2) + 8 * 256;
+    if ((e = cudaMalloc(&ctx->stats_mem, stb)) != cudaSuccess) return bail(e, "cudaMalloc stats");
+    {
+        char* p = static_cast<char*>(ctx->stats_mem);
+        auto take = [&](size_t bytes) {
+            char* r = p;
+            p += (bytes + 255) & ~size_t(255);
+            return r;
+        };
+        ctx->st.episodes = reinterpret_cast<int32_t*>(take(4 * ctx->B));
+        ctx->st.ret = reinterpret_cast<double*>(take(8 * ctx->B));
+        ctx->st.ret_sq = reinterpret_cast<double*>(take(8 * ctx->B));
+        ctx->st.metric = reinterpret_cast<double*>(take(8 * ctx->B));
+        ctx->st.success = reinterpret_cast<double*>(take(8 * ctx->B));
+        ctx->st.min_dist = reinterpret_cast<double*>(take(8 * ctx->B));
+        ctx->st.collisions = reinterpret_cast<int64_t*>(take(8 * ctx->B));
+        ctx->st.qp_inf = reinterpret_cast<int64_t*>(take(8 * ctx->B));
+        cudaMemset(ctx->stats_mem, 0, stb);
+        std::vector<double> inf(ctx->B, INFINITY);
+        cudaMemcpy(ctx->st.min_dist, inf.data(), 8 * ctx->B, cudaMemcpyHostToDevice);
+    }
+    if ((e = cudaMalloc(&ctx->d_err, 16)) != cudaSuccess) return bail(e, "cudaMalloc err");
+    ctx->d_err_serial = reinterpret_cast<long long*>(ctx->d_err + 1);
+    const unsigned long long none = ~0ull;
+    cudaMemcpy(ctx->d_err, &none, sizeof none, cudaMemcpyHostToDevice);
+    cudaMemset(ctx->d_err_serial, 0xff, 8);
+    // launch geometry: persistent grid of (SMs x resident blocks)
+    ctx->smem_group = ctx->fp64 ? mrsim_dev::GroupSmem<double>::bytes(ctx->n, ctx->N)
+                                : mrsim_dev::GroupSmem<float>::bytes(ctx->n, ctx->N);
+    const int smem = ctx->smem_group * (ctx->block / ctx->L);
+    int bps = 0;
+    e = ctx->fp64 ? dispatch_occ<double>(cfg->task, ctx->L, ctx->block, smem, &bps)
+                  : dispatch_occ<float>(cfg->task, ctx->L, ctx->block, smem, &bps);
+    if (e != cudaSuccess) return bail(e, "occupancy query");
+    if (bps < 1) bps = 1;
+    const long long gpb = ctx->block / ctx->L;
+    const long long need = (ctx->B + gpb - 1) / gpb;
+    const long long full = static_cast<long long>(ctx->num_sms) * bps;
+    ctx->grid = static_cast<int>(need < full ? need : full);
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return bail(e, "create sync");
+    *out = ctx;
+    return MRSIM_OK;
+}
+
+void mrsim_destroy(mrsim_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    for (int k = 0; k < 2; ++k) cudaFree(ctx->mem[k]);
+    cudaFree(ctx->stats_mem);
+    cudaFree(ctx->d_err);
+    cudaFree(ctx->d_actions);
+    cudaFree(ctx->d_obs);
+    cudaFree(ctx->d_reward);
+    cudaFree(ctx->d_done);
+    if (ctx->h_actions) cudaFreeHost(ctx->h_actions);
+    delete ctx;
+}
+
+const char* mrsim_last_error(const mrsim_ctx* ctx) { return ctx ? ctx->last_error.c_str() : "null context"; }
+int64_t mrsim_num_envs(const mrsim_ctx* ctx) { return ctx ? ctx->B : 0; }
+
+int mrsim_reset_seeds(mrsim_ctx* ctx, const uint64_t* seeds, float* obs_dev, void* stream) {
+    if (!ctx || !seeds) return set_err(ctx, MRSIM_E_INVALID_ARGUMENT, "reset_batch: seed list is empty");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    uint64_t* d_seeds = nullptr;
+    CK(cudaMalloc(&d_seeds, 8 * ctx->B));
+    CK(cudaMemcpyAsync(d_seeds, seeds, 8 * ctx->B, cudaMemcpyHostToDevice, s));
+    int rc = ctx->fp64 ? do_reset<double>(ctx, ctx->sd, d_seeds, 0, 0, obs_dev, s)
+                       : do_reset<float>(ctx, ctx->sf, d_seeds, 0, 0, obs_dev, s);
+    CK(cudaStreamSynchronize(s));
+    cudaFree(d_seeds);
+    if (rc != MRSIM_OK) return rc;
+    ctx->has_episodes = false;
+    ctx->reset_done = true;
+    return check_device_error(ctx, false);
+}
+
+int mrsim_reset_episodes(mrsim_ctx* ctx, uint64_t root_seed, int64_t first_episode, int64_t episode_stride,
+                         float* obs_dev, void* stream) {
+    if (!ctx || first_episode < 0) return set_err(ctx, MRSIM_E_INVALID_ARGUMENT, "reset: bad episode range");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    ctx->root_seed = root_seed;
+    ctx->episode_stride = episode_stride > 0 ? episode_stride : ctx->B;
+    int rc = ctx->fp64 ? do_reset<double>(ctx, ctx->sd, nullptr, root_seed, first_episode, obs_dev, s)
+                       : do_reset<float>(ctx, ctx->sf, nullptr, root_seed, first_episode, obs_dev, s);
+    CK(cudaStreamSynchronize(s));
+    if (rc != MRSIM_OK) return rc;
+    ctx->has_episodes = true;
+    ctx->reset_done = true;
+    return check_device_error(ctx, false);
+}
+
+int mrsim_step(mrsim_ctx* ctx, const int8_t* actions_dev, float* obs_dev, float* reward_dev, uint8_t* done_dev,
+               float* next_obs_dev, void* stream) {
+    if (!ctx) return MRSIM_E_INVALID_ARGUMENT;
+    if (!ctx->reset_done) return set_err(ctx, MRSIM_E_INVALID_ARGUMENT, "step before reset");
+    if ((ctx->flags & MRSIM_FLAG_AUTO_RESET) && !ctx->has_episodes)
+        return set_err(ctx, MRSIM_E_INVALID_ARGUMENT, "auto-reset needs mrsim_reset_episodes (episode seeds)");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    return ctx->fp64 ? do_step<double>(ctx, ctx->sd, actions_dev, obs_dev, reward_dev, done_dev, next_obs_dev, s)
+                     : do_step<float>(ctx, ctx->sf, actions_dev, obs_dev, reward_dev, done_dev, next_obs_dev, s);
+}
+
+int mrsim_sync(mrsim_ctx* ctx, void* stream) {
+    if (!ctx) return MRSIM_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    return check_device_error(ctx, true);
+}
+
+int mrsim_step_host(mrsim_ctx* ctx, const int32_t* actions_host, float* obs_host, float* reward_host,
+                    uint8_t* done_host, void* stream) {
+    if (!ctx || !actions_host) return MRSIM_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const long long BN = ctx->B * ctx->N;
+    const size_t obs_bytes = sizeof(float) * BN * ctx->D;
+    if (!ctx->d_actions) {
+        CK(cudaMalloc(&ctx->d_actions, BN));
+        CK(cudaMalloc(&ctx->d_obs, obs_bytes));
+        CK(cudaMalloc(&ctx->d_reward, 4 * ctx->B));
+        CK(cudaMalloc(&ctx->d_done, ctx->B));
+        CK(cudaMallocHost(&ctx->h_actions, BN));
+    }
+    // validate_actions (batch.hpp:226-237): sequential, first offender reported
+    for (long long k = 0; k < BN; ++k) {
+        const int a = actions_host[k];
+        if (a < 0 || a >= 5) {
+            char buf[160];
+            std::snprintf(buf, sizeof buf, "step_batch: invalid action %d for environment %lld, robot %lld", a,
+                          k / ctx->N, k % ctx->N);
+            return set_err(ctx, MRSIM_E_INVALID_ARGUMENT, buf);
+        }
+        ctx->h_actions[k] = static_cast<int8_t>(a);
+    }
+    CK(cudaMemcpyAsync(ctx->d_actions, ctx->h_actions, BN, cudaMemcpyHostToDevice, s));
+    int rc = mrsim_step(ctx, ctx->d_actions, obs_host ? ctx->d_obs : nullptr, reward_host ? ctx->d_reward : nullptr,
+                        done_host ? ctx->d_done : nullptr, nullptr, stream);
+    if (rc != MRSIM_OK) return rc;
+    if (obs_host) CK(cudaMemcpyAsync(obs_host, ctx->d_obs, obs_bytes, cudaMemcpyDeviceToHost, s));
+    if (reward_host) CK(cudaMemcpyAsync(reward_host, ctx->d_reward, 4 * ctx->B, cudaMemcpyDeviceToHost, s));
+    if (done_host) CK(cudaMemcpyAsync(done_host, ctx->d_done, ctx->B, cudaMemcpyDeviceToHost, s));
+    return mrsim_sync(ctx, stream);
+}
+
+int mrsim_random_actions(mrsim_ctx* ctx, int8_t* actions_dev, void* stream) {
+    if (!ctx || !actions_dev) return MRSIM_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(ctx->device));
+    const long long total = ctx->B * ctx->N;
+    const int block = 256;
+    const unsigned grid = static_cast<unsigned>((total + block - 1) / block);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (ctx->fp64)
+        mrsim_dev::random_actions_kernel<double><<<grid, block, 0, s>>>(
+            ctx->sd[ctx->cur].step_index, ctx->sd[ctx->cur].pkey, ctx->N, ctx->B, actions_dev);
+    else
+        mrsim_dev::random_actions_kernel<float><<<grid, block, 0, s>>>(
+            ctx->sf[ctx->cur].step_index, ctx->sf[ctx->cur].pkey, ctx->N, ctx->B, actions_dev);
+    CK(cudaGetLastError());
+    return MRSIM_OK;
+}
+
+int mrsim_get_env_states(mrsim_ctx* ctx, int64_t first, int64_t count, mrsim_env_state* out) {
+    if (!ctx || !out || first < 0 || count < 0 || first + count > ctx->B) return MRSIM_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaDeviceSynchronize());
+    cudaError_t e = cudaSuccess;
+    if (ctx->fp64) to_host_states<double>(ctx, ctx->sd[ctx->cur], first, count, out, &e);
+    else to_host_states<float>(ctx, ctx->sf[ctx->cur], first, count, out, &e);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "download state");
+    return MRSIM_OK;
+}
+
+int mrsim_set_env_states(mrsim_ctx* ctx, int64_t first, int64_t count, const mrsim_env_state* in) {
+    if (!ctx || !in || first < 0 || count < 0 || first + count > ctx->B) return MRSIM_E_INVALID_ARGUMENT;
+    for (int64_t k = 0; k < count; ++k)
+        if (in[k].num_robots != ctx->N) return set_err(ctx, MRSIM_E_INVALID_ARGUMENT, "set_env_states: num_robots mismatch");
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaDeviceSynchronize());
+    cudaError_t e = cudaSuccess;
+    if (ctx->fp64) from_host_states<double>(ctx, ctx->sd[ctx->cur], first, count, in, &e);
+    else from_host_states<float>(ctx, ctx->sf[ctx->cur], first, count, in, &e);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "upload state");
+    ctx->reset_done = true;
+    return MRSIM_OK;
+}
+
+int mrsim_get_stats(mrsim_ctx* ctx, mrsim_stats* out) {
+    if (!ctx || !out) return MRSIM_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaDeviceSynchronize());
+    const long long B = ctx->B;
+    std::vector<int32_t> eps(B);
+    std::vector<double> ret(B), ret2(B), met(B), suc(B), mind(B);
+    std::vector<int64_t> col(B), qpi(B);
+    CK(cudaMemcpy(eps.data(), ctx->st.episodes, 4 * B, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(ret.data(), ctx->st.ret, 8 * B, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(ret2.data(), ctx->st.ret_sq, 8 * B, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(met.data(), ctx->st.metric, 8 * B, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(suc.data(), ctx->st.success, 8 * B, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(mind.data(), ctx->st.min_dist, 8 * B, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(col.data(), ctx->st.collisions, 8 * B, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(qpi.data(), ctx->st.qp_inf, 8 * B, cudaMemcpyDeviceToHost));
+    mrsim_stats s;
+    std::memset(&s, 0, sizeof s);
+    s.min_pairwise_distance = INFINITY;
+    for (long long e = 0; e < B; ++e) {
+        s.episodes += eps[e];
+        s.sum_return += ret[e];
+        s.sum_return_sq += ret2[e];
+        s.sum_metric += met[e];
+        s.sum_success += suc[e];
+        s.sum_collisions += col[e];
+        s.sum_qp_infeasible += qpi[e];
+        s.min_pairwise_distance = std::fmin(s.min_pairwise_distance, mind[e]);
+    }
+    s.env_steps = ctx->env_steps;
+    *out = s;
+    return MRSIM_OK;
+}
+
+}  // extern "C"

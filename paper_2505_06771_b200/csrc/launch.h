@@ -1,0 +1,45 @@
+// launch.h — host-side launchers of the per-task kernel instantiations
+// (one translation unit per task, compiled in parallel).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "step_kernel.cuh"
+
+namespace mrsim_host {
+
+template <class Real>
+inline void fill_consts(const mrsim_cfg& c, mrsim_dev::PhysConsts<Real>& k) {
+    const double l = c.projection_distance;
+    k.dt = Real(c.dt);
+    k.v_max = Real(c.v_max);
+    k.w_max = Real(c.omega_max);
+    k.si_max = Real(c.si_max_speed);
+    k.hw = Real(c.arena_half_width);
+    k.hh = Real(c.arena_half_height);
+    k.coll_r = Real(c.collision_radius);
+    k.k_pos = Real(c.k_position);
+    k.l = Real(l);
+    k.gamma = Real(c.barrier_gain);
+    const double r_eff = c.safety_radius + 2.0 * l + c.discrete_margin;  // barrier.hpp:155
+    k.r_eff2 = Real(r_eff * r_eff);
+    const double m_eff = c.boundary_margin + l + c.discrete_margin;  // barrier.hpp:156
+    k.wall_xmin = Real(-c.arena_half_width + m_eff);
+    k.wall_xmax = Real(c.arena_half_width - m_eff);
+    k.wall_ymin = Real(-c.arena_half_height + m_eff);
+    k.wall_ymax = Real(c.arena_half_height - m_eff);
+    const double ro = c.layout.rware_shelf_radius + l + c.discrete_margin;  // barrier.hpp:157
+    k.obs_r_eff2 = Real(ro * ro);
+    k.cap = Real(c.v_max + l * c.omega_max + 0.1);  // barrier.hpp:173
+    k.tol = mrsim_dev::Prec<Real>::tol;
+}
+
+template <class Real, int TASK>
+cudaError_t launch_step(const mrsim_dev::StepParams<Real>& p, int L, int grid, int block, int smem,
+                        cudaStream_t stream);
+template <class Real, int TASK>
+cudaError_t step_occupancy(int L, int block, int smem, int* blocks_per_sm);
+template <class Real, int TASK>
+cudaError_t launch_reset(const mrsim_dev::ResetParams<Real>& p, cudaStream_t stream);
+
+}  // namespace mrsim_host

@@ -1,0 +1,217 @@
+// mrsim_device.cuh — device-side building blocks shared by every kernel:
+// the flattened per-launch parameter block, the counter-based SplitMix64
+// RNG (bit-exact with rng.hpp), sub-warp group collectives, and small
+// math helpers templated on the compute precision.
+//
+// Reference paths below are relative to /root/reference/proj/include/mrsim.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "mrsim_cuda.h"
+
+namespace mrsim_dev {
+
+// ---------------------------------------------------------------------------
+// Precision traits. fp64 mirrors the reference's tolerances exactly
+// (qp.hpp:183 tolerance 1e-9, qp.hpp:71/115/248/304 pivots 1e-14, 295 r>1e-12);
+// fp32 scales them to its unit roundoff (rows are unit-norm, |u| <= 0.48).
+// ---------------------------------------------------------------------------
+template <class Real>
+struct Prec;
+template <>
+struct Prec<float> {
+    static constexpr float tol = 2e-6f;       // accepted constraint violation
+    static constexpr float eps_z = 1e-10f;    // |z|^2 below which the new normal is dependent
+    static constexpr float eps_r = 1e-6f;     // r_a > eps_r counts as a blocking multiplier
+    static constexpr float eps_row = 1e-14f;  // zero-row threshold of fold_rows
+};
+template <>
+struct Prec<double> {
+    static constexpr double tol = 1e-9;
+    static constexpr double eps_z = 1e-14;
+    static constexpr double eps_r = 1e-12;
+    static constexpr double eps_row = 1e-14;
+};
+
+__device__ __forceinline__ float dsqrt(float x) { return sqrtf(x); }
+__device__ __forceinline__ double dsqrt(double x) { return sqrt(x); }
+__device__ __forceinline__ float dhypot(float a, float b) { return hypotf(a, b); }
+__device__ __forceinline__ double dhypot(double a, double b) { return hypot(a, b); }
+__device__ __forceinline__ void dsincos(float x, float* s, float* c) { sincosf(x, s, c); }
+__device__ __forceinline__ void dsincos(double x, double* s, double* c) { sincos(x, s, c); }
+__device__ __forceinline__ float dabs(float x) { return fabsf(x); }
+__device__ __forceinline__ double dabs(double x) { return fabs(x); }
+template <class T>
+__device__ __forceinline__ T dmin(T a, T b) { return a < b ? a : b; }
+template <class T>
+__device__ __forceinline__ T dmax(T a, T b) { return a > b ? a : b; }
+// core.hpp:144 clamp(v, lo, hi) = min(max(v, lo), hi)
+template <class T>
+__device__ __forceinline__ T dclamp(T v, T lo, T hi) { return dmin(dmax(v, lo), hi); }
+
+template <class Real>
+struct Consts;
+template <>
+struct Consts<float> {
+    static constexpr float pi = 3.14159265358979323846f;
+    static constexpr float two_pi = 6.28318530717958647692f;
+    static constexpr float inf = __builtin_huge_valf();
+};
+template <>
+struct Consts<double> {
+    static constexpr double pi = 3.14159265358979323846;
+    static constexpr double two_pi = 6.28318530717958647692;
+    static constexpr double inf = __builtin_huge_val();
+};
+
+// ---------------------------------------------------------------------------
+// SplitMix64 counter RNG (rng.hpp:15-67). Pure integer math => bit-exact.
+// ---------------------------------------------------------------------------
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ULL;
+constexpr uint64_t kForkSalt = 0x632BE59BD9B4E019ULL;
+constexpr uint64_t kEpisodeTag = 0xE915E915E915E915ULL;  // harness.hpp:22
+constexpr uint64_t kPolicyTag = 0x9D0C7E5F00000001ULL;   // harness.hpp:23
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {  // rng.hpp:17-21
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t key_from_seed(uint64_t seed) {  // rng.hpp:29-31
+    return mix64(seed + kGamma);
+}
+__host__ __device__ __forceinline__ uint64_t fork_key(uint64_t key, uint64_t tag) {  // rng.hpp:35-37
+    return mix64(key ^ mix64(tag * kGamma + kForkSalt));
+}
+// harness.hpp:25-27
+__host__ __device__ __forceinline__ uint64_t derive_episode_seed(uint64_t root, int64_t episode) {
+    return fork_key(fork_key(key_from_seed(root), kEpisodeTag),
+                    static_cast<uint64_t>(static_cast<int>(episode)));
+}
+
+struct Rng {  // SplitRng{key, ctr} (rng.hpp:25-67)
+    uint64_t key;
+    uint64_t ctr;
+    __device__ __forceinline__ uint64_t next_u64() {  // rng.hpp:39-42
+        ++ctr;
+        return mix64(key + ctr * kGamma);
+    }
+    __device__ __forceinline__ double uniform() {  // rng.hpp:45-47
+        return static_cast<double>(next_u64() >> 11) * 0x1.0p-53;
+    }
+    __device__ __forceinline__ double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+    __device__ __forceinline__ uint64_t uniform_int(uint64_t n) {  // rng.hpp:52-55 (128-bit mulhi)
+        return __umul64hi(next_u64(), n);
+    }
+    __device__ __forceinline__ double normal() {  // rng.hpp:59-64
+        double u1 = uniform();
+        double u2 = uniform();
+        if (u1 <= 0.0) u1 = 0x1.0p-53;
+        return sqrt(-2.0 * log(u1)) * cos(2.0 * 3.14159265358979323846 * u2);
+    }
+};
+
+// policy_stream(seed, step, robot).uniform_int(5) (harness.hpp:29-34, policy.hpp:448-449),
+// with the per-episode prefix from_seed(seed).fork(kPolicyTag) precomputed.
+__device__ __forceinline__ int policy_action(uint64_t policy_key, int step, int robot) {
+    uint64_t k = fork_key(fork_key(policy_key, static_cast<uint64_t>(step)), static_cast<uint64_t>(robot));
+    return static_cast<int>(__umul64hi(mix64(k + kGamma), 5ULL));
+}
+__host__ __device__ __forceinline__ uint64_t policy_key_of(uint64_t seed) {
+    return fork_key(key_from_seed(seed), kPolicyTag);
+}
+
+// ---------------------------------------------------------------------------
+// Sub-warp group of L lanes cooperating on one environment.
+// ---------------------------------------------------------------------------
+template <int L>
+struct Group {
+    static_assert(L == 8 || L == 16 || L == 32, "group size");
+    unsigned mask;
+    int lane;  // 0..L-1
+    __device__ __forceinline__ Group() {
+        const int wl = threadIdx.x & 31;
+        lane = wl & (L - 1);
+        mask = (L == 32) ? 0xffffffffu : (((1u << L) - 1u) << (wl & ~(L - 1)));
+    }
+    __device__ __forceinline__ void sync() const { __syncwarp(mask); }
+    template <class T>
+    __device__ __forceinline__ T shfl(T v, int src) const { return __shfl_sync(mask, v, src, L); }
+    template <class T>
+    __device__ __forceinline__ T sum(T v) const {
+#pragma unroll
+        for (int o = L / 2; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o, L);
+        return v;
+    }
+    template <class T>
+    __device__ __forceinline__ T min(T v) const {
+#pragma unroll
+        for (int o = L / 2; o > 0; o >>= 1) {
+            T w = __shfl_xor_sync(mask, v, o, L);
+            v = w < v ? w : v;
+        }
+        return v;
+    }
+    template <class T>
+    __device__ __forceinline__ T max(T v) const {
+#pragma unroll
+        for (int o = L / 2; o > 0; o >>= 1) {
+            T w = __shfl_xor_sync(mask, v, o, L);
+            v = w > v ? w : v;
+        }
+        return v;
+    }
+    __device__ __forceinline__ bool any(bool p) const { return (__ballot_sync(mask, p) & mask) != 0u; }
+    __device__ __forceinline__ unsigned ballot(bool p) const {
+        const unsigned b = __ballot_sync(mask, p) & mask;
+        return (L == 32) ? b : (b >> ((threadIdx.x & 31) & ~(L - 1)));
+    }
+    // argmax with ties to the lowest index (first-maximal semantics of the
+    // reference's `v > worst` scans, qp.hpp:228-238). idx < 0 means "none".
+    template <class T>
+    __device__ __forceinline__ void argmax(T& v, int& idx) const {
+#pragma unroll
+        for (int o = L / 2; o > 0; o >>= 1) {
+            T ov = __shfl_xor_sync(mask, v, o, L);
+            int oi = __shfl_xor_sync(mask, idx, o, L);
+            const bool take = (oi >= 0) && (idx < 0 || ov > v || (ov == v && oi < idx));
+            if (take) { v = ov; idx = oi; }
+        }
+    }
+    // argmin with ties to the lowest index (`t < t1`, qp.hpp:294-302).
+    template <class T>
+    __device__ __forceinline__ void argmin(T& v, int& idx) const {
+#pragma unroll
+        for (int o = L / 2; o > 0; o >>= 1) {
+            T ov = __shfl_xor_sync(mask, v, o, L);
+            int oi = __shfl_xor_sync(mask, idx, o, L);
+            const bool take = (oi >= 0) && (idx < 0 || ov < v || (ov == v && oi < idx));
+            if (take) { v = ov; idx = oi; }
+        }
+    }
+};
+
+// ---------------------------------------------------------------------------
+// Device error word: the first (lowest env) error wins, mirroring the
+// reference's sequential validation order (batch.hpp:226-237).
+// code layout: [env:40][robot:8][code:8] in a u64 for atomicMin.
+// ---------------------------------------------------------------------------
+enum DevErr : unsigned {
+    kErrInvalidAction = 1,   // invalid_argument: step_batch: invalid action
+    kErrCoincident = 2,      // domain_error: coincident robot positions
+    kErrNonFinite = 3,       // domain_error: wrap_angle non-finite
+    kErrSpawn = 4,           // runtime_error: sample_poses could not place robot
+    kErrGoals = 5,           // runtime_error: navigation could not place goals
+    kErrPrey = 6,            // runtime_error: predator_prey could not place prey
+};
+__device__ __forceinline__ void report_error(unsigned long long* err, long long env, int robot, unsigned code,
+                                             int detail = 0) {
+    unsigned long long v = (static_cast<unsigned long long>(env) << 24) |
+                           (static_cast<unsigned long long>(robot & 0xff) << 16) |
+                           (static_cast<unsigned long long>(detail & 0xff) << 8) | (code & 0xff);
+    atomicMin(err, v);
+}
+
+}  // namespace mrsim_dev

@@ -1,0 +1,272 @@
+// unit_kernels.cu — unit-level entry points of the hot-path pieces, used by
+// the parity tests against the reference's own QP / barrier tests:
+//   mrsim_qp_solve_batch      <- solve_qp (qp.hpp:183-357), one warp per QP
+//   mrsim_apply_barrier_batch <- apply_barrier (barrier.hpp:132-205), one group per team
+// Both run the same device code as the fused step kernel (qp_solve_group,
+// barrier_filter).
+#include <cstring>
+#include <vector>
+
+#include "launch.h"
+#include "mrsim_cuda.h"
+
+namespace mrsim_dev {
+
+constexpr int kQpMaxN = 32;
+constexpr int kQpMaxM = 64;
+
+template <class Real>
+__global__ void __launch_bounds__(32) qp_batch_kernel(int count, int n, int m, const double* A, const double* b,
+                                                      const double* lo, const double* hi, const double* unom,
+                                                      double tol, double* u_out, int32_t* status_out,
+                                                      int32_t* iters_out) {
+    const int t = blockIdx.x;
+    if (t >= count) return;
+    __shared__ Real G[kQpMaxM * kQpMaxN];
+    __shared__ Real h[kQpMaxM];
+    __shared__ Real ush[kQpMaxN], los[kQpMaxN], his[kQpMaxN];
+    __shared__ Real wsr[QpSmem<Real>::reals(kQpMaxN)];
+    __shared__ int wsi[QpSmem<Real>::ints(kQpMaxN)];
+    const Group<32> g;
+    const int lane = g.lane;
+    const double* At = A + static_cast<size_t>(t) * m * n;
+    // fold_rows (qp.hpp:104-141): normalise; zero rows keep b unnormalised
+    for (int r = lane; r < m; r += 32) {
+        double norm = 0.0;
+        for (int i = 0; i < n; ++i) norm += At[r * n + i] * At[r * n + i];
+        norm = sqrt(norm);
+        const double br = b[static_cast<size_t>(t) * m + r];
+        if (norm < 1e-14) {
+            for (int i = 0; i < n; ++i) G[r * n + i] = Real(0);
+            h[r] = Real(br);
+        } else {
+            for (int i = 0; i < n; ++i) G[r * n + i] = Real(At[r * n + i] / norm);
+            h[r] = Real(br / norm);
+        }
+    }
+    if (lane < n) {
+        los[lane] = Real(lo[static_cast<size_t>(t) * n + lane]);
+        his[lane] = Real(hi[static_cast<size_t>(t) * n + lane]);
+    }
+    g.sync();
+    int boxes = 0;
+    for (int i = 0; i < n; ++i) {
+        boxes += hi[static_cast<size_t>(t) * n + i] < 1e30 ? 1 : 0;
+        boxes += lo[static_cast<size_t>(t) * n + i] > -1e30 ? 1 : 0;
+    }
+    QpSmem<Real> ws;
+    ws.carve(wsr, wsi, n);
+    DenseRows<Real, 32, kQpMaxM> rows{G, h, ush, los, his, n, m, 0ull, 0u};
+    Real u = lane < n ? Real(unom[static_cast<size_t>(t) * n + lane]) : Real(0);
+    int iters = 0;
+    const int status = qp_solve_group<Real, 32>(g, rows, ws, n, u, m + boxes, 0, Real(tol), &iters);
+    if (lane < n) u_out[static_cast<size_t>(t) * n + lane] = double(u);
+    if (lane == 0) {
+        status_out[t] = status;
+        iters_out[t] = iters;
+    }
+}
+
+template <class Real, int L>
+__global__ void __launch_bounds__(256) barrier_batch_kernel(const __grid_constant__ mrsim_cfg c, PhysConsts<Real> k,
+                                                            int count, int N, const double* poses,
+                                                            const double* nominal, int nobs, const double* obstacles,
+                                                            const uint64_t* masks, double* cmds, int32_t* infeasible,
+                                                            int32_t* coincident, int smem_group) {
+    constexpr int MAXPAIR = LaneCfg<L>::kMaxPair;
+    constexpr int MAXOBS = MRSIM_MAX_SLOTS / 2;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const Group<L> g;
+    const int lane = g.lane;
+    const int gib = threadIdx.x / L;
+    const long long t = static_cast<long long>(blockIdx.x) * (blockDim.x / L) + gib;
+    if (t >= count) return;
+    const int n = 2 * N, P = N * (N - 1) / 2;
+    QpSmem<Real> ws;
+    Real* wr = reinterpret_cast<Real*>(smem_raw + gib * smem_group);
+    ws.carve(wr, reinterpret_cast<int*>(wr + QpSmem<Real>::reals(n)), n);
+    const bool vlane = lane < n;
+    const int ri = vlane ? lane >> 1 : 0;
+    const int ax = lane & 1;
+    const double* ps = poses + t * N * 3;
+    const double* nm = nominal + t * N * 2;
+    Real x = 0, y = 0, th = 0, nv = 0, nw = 0;
+    if (vlane) {
+        x = Real(ps[3 * ri]);
+        y = Real(ps[3 * ri + 1]);
+        th = Real(ps[3 * ri + 2]);
+        nv = dclamp(Real(nm[2 * ri]), -k.v_max, k.v_max);  // clamp_command (barrier.hpp:142)
+        nw = dclamp(Real(nm[2 * ri + 1]), -k.w_max, k.w_max);
+    }
+    Real cv = nv, cw = nw;
+    int status = kQpOptimal;
+    if (c.barrier_enabled) {
+        BarrierRows<Real, L, MAXPAIR, MAXOBS> rows;
+        rows.N = N;
+        rows.n = n;
+        rows.P = P;
+        rows.off_obs = P + 4 * N;
+        rows.off_box = rows.off_obs + N * MRSIM_MAX_SLOTS;
+        rows.cap = k.cap;
+#pragma unroll
+        for (int s = 0; s < MAXPAIR; ++s) {
+            const int pidx = lane + s * L;
+            int i = 0, j = 0;
+            if (pidx < P) pair_of(pidx, N, i, j);
+            rows.pi[s] = i;
+            rows.pj[s] = j;
+        }
+        // static obstacles with masks (barrier.hpp:106-119), radius inflated (barrier.hpp:157)
+        rows.nob = 0;
+        int obs_rows = 0;
+        const double infl = c.projection_distance + c.discrete_margin;
+        for (int o = 0; o < nobs; ++o) {
+            const uint64_t mk = masks ? masks[t * nobs + o] : 0ull;
+            for (int i = 0; i < N; ++i) {
+                if (mk != 0 && ((mk >> i) & 1ull) == 0) continue;
+                ++obs_rows;
+                if (vlane && i == ri && (o & 1) == ax) {
+                    const double* ob = obstacles + (t * nobs + o) * 3;
+                    const double r = ob[2] + infl;
+#pragma unroll
+                    for (int q = 0; q < MAXOBS; ++q)
+                        if (q == rows.nob) {
+                            rows.oslot[q] = o;
+                            rows.ocx[q] = Real(ob[0]);
+                            rows.ocy[q] = Real(ob[1]);
+                            rows.or2[q] = Real(r * r);
+                        }
+                    ++rows.nob;
+                }
+            }
+        }
+        Real sn, cs;
+        dsincos(th, &sn, &cs);
+        const Real prx = x + cs * k.l, pry = y + sn * k.l;
+        status = barrier_filter<Real, L>(g, rows, ws, k, n, P, vlane, ax, ri, prx, pry, cs, sn, nv, nw,
+                                         P + 4 * N + obs_rows + 2 * n, cv, cw);
+    }
+    if (vlane && ax == 0) {
+        cmds[(t * N + ri) * 2] = double(cv);
+        cmds[(t * N + ri) * 2 + 1] = double(cw);
+    }
+    if (lane == 0) {
+        infeasible[t] = status == kQpInfeasible ? 1 : 0;
+        coincident[t] = status < 0 ? 1 : 0;
+    }
+}
+
+}  // namespace mrsim_dev
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    ~DevBuf() { cudaFree(p); }
+};
+
+template <class T>
+cudaError_t upload(DevBuf& d, const T* h, size_t count) {
+    cudaError_t e = cudaMalloc(&d.p, sizeof(T) * (count > 0 ? count : 1));
+    if (e != cudaSuccess || count == 0 || !h) return e;
+    return cudaMemcpy(d.p, h, sizeof(T) * count, cudaMemcpyHostToDevice);
+}
+
+template <class Real, int L>
+cudaError_t run_barrier(const mrsim_cfg& c, int count, const double* dp, const double* dn, int nobs,
+                        const double* dobs, const uint64_t* dm, double* dc, int32_t* di, int32_t* dco) {
+    mrsim_dev::PhysConsts<Real> k;
+    mrsim_host::fill_consts(c, k);
+    const int N = c.num_robots;
+    const int block = 256;
+    const int gpb = block / L;
+    const int sg = ((mrsim_dev::QpSmem<Real>::reals(2 * N) * static_cast<int>(sizeof(Real)) +
+                     mrsim_dev::QpSmem<Real>::ints(2 * N) * 4) + 15) & ~15;
+    const int grid = (count + gpb - 1) / gpb;
+    auto kern = mrsim_dev::barrier_batch_kernel<Real, L>;
+    if (sg * gpb > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sg * gpb);
+    kern<<<grid, block, sg * gpb>>>(c, k, count, N, dp, dn, nobs, dobs, dm, dc, di, dco, sg);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+extern "C" {
+
+int mrsim_qp_solve_batch(int device, int fp64, int count, int n, int m, const double* A, const double* b,
+                         const double* lo, const double* hi, const double* u_nom, double tolerance, double* u_out,
+                         int32_t* status_out, int32_t* iterations_out) {
+    if (count < 1 || n < 1 || n > mrsim_dev::kQpMaxN || m < 0 || m > mrsim_dev::kQpMaxM)
+        return MRSIM_E_INVALID_ARGUMENT;
+    if (cudaSetDevice(device) != cudaSuccess) return MRSIM_E_CUDA;
+    DevBuf dA, db, dlo, dhi, du, dout, dst, dit;
+    cudaError_t e = cudaSuccess;
+    if ((e = upload(dA, A, static_cast<size_t>(count) * m * n)) != cudaSuccess) return MRSIM_E_CUDA;
+    if ((e = upload(db, b, static_cast<size_t>(count) * m)) != cudaSuccess) return MRSIM_E_CUDA;
+    if ((e = upload(dlo, lo, static_cast<size_t>(count) * n)) != cudaSuccess) return MRSIM_E_CUDA;
+    if ((e = upload(dhi, hi, static_cast<size_t>(count) * n)) != cudaSuccess) return MRSIM_E_CUDA;
+    if ((e = upload(du, u_nom, static_cast<size_t>(count) * n)) != cudaSuccess) return MRSIM_E_CUDA;
+    if ((e = upload<double>(dout, nullptr, static_cast<size_t>(count) * n)) != cudaSuccess) return MRSIM_E_CUDA;
+    if ((e = upload<int32_t>(dst, nullptr, count)) != cudaSuccess) return MRSIM_E_CUDA;
+    if ((e = upload<int32_t>(dit, nullptr, count)) != cudaSuccess) return MRSIM_E_CUDA;
+    if (fp64)
+        mrsim_dev::qp_batch_kernel<double><<<count, 32>>>(
+            count, n, m, static_cast<double*>(dA.p), static_cast<double*>(db.p), static_cast<double*>(dlo.p),
+            static_cast<double*>(dhi.p), static_cast<double*>(du.p), tolerance, static_cast<double*>(dout.p),
+            static_cast<int32_t*>(dst.p), static_cast<int32_t*>(dit.p));
+    else
+        mrsim_dev::qp_batch_kernel<float><<<count, 32>>>(
+            count, n, m, static_cast<double*>(dA.p), static_cast<double*>(db.p), static_cast<double*>(dlo.p),
+            static_cast<double*>(dhi.p), static_cast<double*>(du.p), tolerance, static_cast<double*>(dout.p),
+            static_cast<int32_t*>(dst.p), static_cast<int32_t*>(dit.p));
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return MRSIM_E_CUDA;
+    cudaMemcpy(u_out, dout.p, sizeof(double) * count * n, cudaMemcpyDeviceToHost);
+    cudaMemcpy(status_out, dst.p, sizeof(int32_t) * count, cudaMemcpyDeviceToHost);
+    if (iterations_out) cudaMemcpy(iterations_out, dit.p, sizeof(int32_t) * count, cudaMemcpyDeviceToHost);
+    return cudaGetLastError() == cudaSuccess ? MRSIM_OK : MRSIM_E_CUDA;
+}
+
+int mrsim_apply_barrier_batch(int device, int fp64, const mrsim_cfg* cfg, int count, const double* poses,
+                              const double* nominal, int num_obstacles, const double* obstacles,
+                              const uint64_t* obstacle_masks, double* commands_out, int32_t* infeasible_out) {
+    if (!cfg || count < 1 || num_obstacles < 0 || num_obstacles > MRSIM_MAX_SLOTS) return MRSIM_E_INVALID_ARGUMENT;
+    const int N = cfg->num_robots;
+    if (N < 1 || N > MRSIM_MAX_ROBOTS) return MRSIM_E_UNSUPPORTED;
+    if (cudaSetDevice(device) != cudaSuccess) return MRSIM_E_CUDA;
+    DevBuf dp, dn, dobs, dm, dc, di, dco;
+    if (upload(dp, poses, static_cast<size_t>(count) * N * 3) != cudaSuccess) return MRSIM_E_CUDA;
+    if (upload(dn, nominal, static_cast<size_t>(count) * N * 2) != cudaSuccess) return MRSIM_E_CUDA;
+    if (upload(dobs, obstacles, static_cast<size_t>(count) * num_obstacles * 3) != cudaSuccess) return MRSIM_E_CUDA;
+    if (upload(dm, obstacle_masks, static_cast<size_t>(count) * num_obstacles) != cudaSuccess) return MRSIM_E_CUDA;
+    if (upload<double>(dc, nullptr, static_cast<size_t>(count) * N * 2) != cudaSuccess) return MRSIM_E_CUDA;
+    if (upload<int32_t>(di, nullptr, count) != cudaSuccess) return MRSIM_E_CUDA;
+    if (upload<int32_t>(dco, nullptr, count) != cudaSuccess) return MRSIM_E_CUDA;
+    const double* P_ = static_cast<double*>(dp.p);
+    const double* N_ = static_cast<double*>(dn.p);
+    const double* O_ = static_cast<double*>(dobs.p);
+    const uint64_t* M_ = obstacle_masks ? static_cast<uint64_t*>(dm.p) : nullptr;
+    double* C_ = static_cast<double*>(dc.p);
+    int32_t* I_ = static_cast<int32_t*>(di.p);
+    int32_t* X_ = static_cast<int32_t*>(dco.p);
+    cudaError_t e;
+    const int n = 2 * N;
+    if (fp64) {
+        if (n <= 8) e = run_barrier<double, 8>(*cfg, count, P_, N_, num_obstacles, O_, M_, C_, I_, X_);
+        else if (n <= 16) e = run_barrier<double, 16>(*cfg, count, P_, N_, num_obstacles, O_, M_, C_, I_, X_);
+        else e = run_barrier<double, 32>(*cfg, count, P_, N_, num_obstacles, O_, M_, C_, I_, X_);
+    } else {
+        if (n <= 8) e = run_barrier<float, 8>(*cfg, count, P_, N_, num_obstacles, O_, M_, C_, I_, X_);
+        else if (n <= 16) e = run_barrier<float, 16>(*cfg, count, P_, N_, num_obstacles, O_, M_, C_, I_, X_);
+        else e = run_barrier<float, 32>(*cfg, count, P_, N_, num_obstacles, O_, M_, C_, I_, X_);
+    }
+    if (e != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) return MRSIM_E_CUDA;
+    std::vector<int32_t> co(count);
+    cudaMemcpy(commands_out, C_, sizeof(double) * count * N * 2, cudaMemcpyDeviceToHost);
+    cudaMemcpy(infeasible_out, I_, sizeof(int32_t) * count, cudaMemcpyDeviceToHost);
+    cudaMemcpy(co.data(), X_, sizeof(int32_t) * count, cudaMemcpyDeviceToHost);
+    for (int t = 0; t < count; ++t)
+        if (co[t]) return MRSIM_E_DOMAIN;  // coincident robot positions (barrier.hpp:73-74)
+    return MRSIM_OK;
+}
+
+}  // extern "C"
