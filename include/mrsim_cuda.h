@@ -232,6 +232,9 @@ int mrsim_config_validate(const mrsim_cfg* cfg, char* message, int message_len);
 /* Per-robot observation length after het_augment (batch.hpp:143-151). */
 int mrsim_obs_dim(const mrsim_cfg* cfg);
 const char* mrsim_task_name(int task);
+/* Per-env task-state words kept in HBM: nf compute-precision fields and ni
+ * 32-bit integer words (used for the algorithmic-bytes roofline model). */
+int mrsim_task_fields(const mrsim_cfg* cfg, int* nf, int* ni);
 
 /* ---- batched environments on one device ---- */
 

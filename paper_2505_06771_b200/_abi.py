@@ -89,6 +89,7 @@ FUNCTIONS = {
     "mrsim_config_validate": (ctypes.c_int, [P(Cfg), ctypes.c_char_p, ctypes.c_int]),
     "mrsim_obs_dim": (ctypes.c_int, [P(Cfg)]),
     "mrsim_task_name": (ctypes.c_char_p, [ctypes.c_int]),
+    "mrsim_task_fields": (ctypes.c_int, [P(Cfg), P(ctypes.c_int), P(ctypes.c_int)]),
     "mrsim_create": (ctypes.c_int, [P(Cfg), ctypes.c_int, ctypes.c_int64, ctypes.c_uint32, P(c_void_p)]),
     "mrsim_destroy": (None, [c_void_p]),
     "mrsim_last_error": (ctypes.c_char_p, [c_void_p]),

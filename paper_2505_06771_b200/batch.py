@@ -92,6 +92,11 @@ class ScenarioConfig:
     def obs_dim(self) -> int:
         return lib().mrsim_obs_dim(ctypes.byref(self.raw))
 
+    def task_fields(self) -> tuple[int, int]:
+        nf, ni = ctypes.c_int(), ctypes.c_int()
+        lib().mrsim_task_fields(ctypes.byref(self.raw), ctypes.byref(nf), ctypes.byref(ni))
+        return nf.value, ni.value
+
     def heterogeneity(self) -> np.ndarray:
         return np.array([[self.raw.het[i][k] for k in range(self.raw.het_cols)]
                          for i in range(self.raw.het_rows)], dtype=np.float64)

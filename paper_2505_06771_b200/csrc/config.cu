@@ -410,4 +410,10 @@ int mrsim_config_validate(const mrsim_cfg* cp, char* msg, int len) {
 
 int mrsim_obs_dim(const mrsim_cfg* c) { return c ? mrsim_dev::obs_dim_of(*c) : -1; }
 
+int mrsim_task_fields(const mrsim_cfg* c, int* nf, int* ni) {
+    if (!c || !nf || !ni) return MRSIM_E_INVALID_ARGUMENT;
+    mrsim_dev::task_fields(*c, nf, ni);
+    return MRSIM_OK;
+}
+
 }  // extern "C"
