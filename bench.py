@@ -8,7 +8,10 @@ in-kernel auto-reset with the harness's wave seeding. One "step" = one
 batched env-step of every env (10 physics ticks each).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--task navigation --robots 4 --envs 65536] [--fp64]
+                  [--task navigation --robots 4 --envs 65536] [--fp32]
+
+The product path computes in fp64 (bit-exact discrete outcomes vs the
+reference); --fp32 selects the fast mode.
 
 Under torchrun each rank drives one GPU with its own contiguous env slice
 (weak scaling, no collective in the step); the only cross-GPU traffic is the
@@ -41,14 +44,15 @@ ARCTIC_SPAWN = [-1.55, -1.05, -0.9, 0.9]
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--task", default="navigation")
     ap.add_argument("--robots", type=int, default=4)
     ap.add_argument("--envs", type=int, default=65536, help="envs per GPU")
     ap.add_argument("--max-steps", type=int, default=70)
-    ap.add_argument("--fp64", action="store_true")
+    ap.add_argument("--fp32", action="store_true",
+                    help="opt-in fp32 fast mode (forks from the reference at hold-rule near-ties)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
     ap.add_argument("--e2e-steps", type=int, default=20)
@@ -184,7 +188,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = build_cfg(a)
     B = a.envs
-    batch = m.CudaEnvBatch(cfg, B, device=local, fp64=a.fp64, auto_reset=True)
+    batch = m.CudaEnvBatch(cfg, B, device=local, fp64=(not a.fp32), auto_reset=True)
     batch.reset_episodes(root_seed=0, first_episode=rank * B, episode_stride=world * B)
     stream = torch.cuda.current_stream()
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
@@ -233,7 +237,7 @@ def main():
     if a.e2e_steps > 0:
         rng = np.random.default_rng(rank)
         acts = rng.integers(0, 5, size=(a.e2e_steps, B, a.robots), dtype=np.int32)
-        hb = m.CudaEnvBatch(cfg, B, device=local, fp64=a.fp64, auto_reset=True)
+        hb = m.CudaEnvBatch(cfg, B, device=local, fp64=(not a.fp32), auto_reset=True)
         hb.reset_episodes(root_seed=0, first_episode=rank * B, episode_stride=world * B)
         hb.step_host(acts[0])
         if dist:
@@ -257,16 +261,17 @@ def main():
         if os.path.exists(pk):
             peaks = json.load(open(pk))
         hbm_peak = peaks.get("hbm_gbs", 6650.0)
-        bpe = algorithmic_bytes_per_env_step(cfg, a.fp64)
+        bpe = algorithmic_bytes_per_env_step(cfg, (not a.fp32))
         fpe = algorithmic_flops_per_env_step(cfg)
         per_gpu = value / world
         achieved_gbs = per_gpu * bpe / 1e9
-        fp32_peak = 148 * 128 * 2 * (clk["sm_max_mhz"] if clk else 1965.0) * 1e6 / 1e12
+        fp64 = not a.fp32
+        pipe_peak = m.lib().mrsim_probe_fma_peak(local, int(fp64)) / 1e12  # measured FMA-chain peak
         traffic = None
         tf = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tf):
             try:
-                traffic = json.load(open(tf)).get(f"{a.task}{a.robots}_{'fp64' if a.fp64 else 'fp32'}")
+                traffic = json.load(open(tf)).get(f"{a.task}{a.robots}_{'fp64' if (not a.fp32) else 'fp32'}")
             except Exception:
                 traffic = None
         cpu = None
@@ -284,7 +289,7 @@ def main():
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,
-            "dtype": "f64" if a.fp64 else "f32",
+            "dtype": "f64" if (not a.fp32) else "f32",
             "data": "synthetic: harness random policy on device, derive_episode_seed(0, e) resets",
             "config": {"workload": workload_name(a), "task": a.task, "robots": a.robots, "envs_per_gpu": B,
                        "global_envs": B * world, "max_steps": a.max_steps, "sub_steps": cfg.raw.sub_steps,
@@ -293,10 +298,11 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved_gbs / hbm_peak, "traffic": traffic,
                          "algorithmic_bytes_per_env_step": bpe, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
-                         "fp32": {"achieved_tflops": per_gpu * fpe / 1e12, "peak_tflops": fp32_peak,
-                                  "frac": per_gpu * fpe / 1e12 / fp32_peak,
+                         "pipe": {"pipe": "fp64" if fp64 else "fp32",
+                                  "achieved_tflops": per_gpu * fpe / 1e12, "peak_tflops": pipe_peak,
+                                  "frac": per_gpu * fpe / 1e12 / pipe_peak,
                                   "algorithmic_flops_per_env_step": fpe,
-                                  "peak_source": "148 SM x 128 FP32 lanes x 2 x sm_max_mhz (nominal)"}},
+                                  "peak_source": "measured FMA-chain probe (mrsim_probe_fma_peak) on this GPU"}},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": a.steps,

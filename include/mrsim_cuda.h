@@ -306,6 +306,12 @@ int mrsim_apply_barrier_batch(int device, int fp64, const mrsim_cfg* cfg, int co
                               const double* obstacles, const uint64_t* obstacle_masks,
                               double* commands_out, int32_t* infeasible_out);
 
+/* ---- measurement probe (roofline denominator) ---- */
+
+/* Sustained FMA throughput of this device in FLOP/s (2 per FMA), fp64 or
+ * fp32, from a register-resident FMA-chain kernel over all SMs. */
+double mrsim_probe_fma_peak(int device, int fp64);
+
 #ifdef __cplusplus
 }
 #endif

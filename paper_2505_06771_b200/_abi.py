@@ -109,6 +109,7 @@ FUNCTIONS = {
                                             P(ctypes.c_double), P(ctypes.c_double), P(ctypes.c_double),
                                             P(ctypes.c_double), P(ctypes.c_double), ctypes.c_double,
                                             P(ctypes.c_double), P(ctypes.c_int32), P(ctypes.c_int32)]),
+    "mrsim_probe_fma_peak": (ctypes.c_double, [ctypes.c_int, ctypes.c_int]),
     "mrsim_apply_barrier_batch": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, P(Cfg), ctypes.c_int,
                                                  P(ctypes.c_double), P(ctypes.c_double), ctypes.c_int,
                                                  P(ctypes.c_double), P(ctypes.c_uint64), P(ctypes.c_double),

@@ -135,7 +135,7 @@ def _stream_handle(stream) -> ctypes.c_void_p:
 class CudaEnvBatch:
     """B environments stepped in lockstep on one GPU (one mrsim_ctx)."""
 
-    def __init__(self, cfg: ScenarioConfig, num_envs: int, device: int = 0, fp64: bool = False,
+    def __init__(self, cfg: ScenarioConfig, num_envs: int, device: int = 0, fp64: bool = True,
                  auto_reset: bool = False):
         cfg.validate()
         self.cfg = cfg.copy()
@@ -242,7 +242,7 @@ class CudaEnvBatch:
         return {f: getattr(s, f) for f, _ in _abi.Stats._fields_}
 
 
-def reset_batch(cfg: ScenarioConfig, seeds, device: int = 0, fp64: bool = False):
+def reset_batch(cfg: ScenarioConfig, seeds, device: int = 0, fp64: bool = True):
     """reset_batch (batch.hpp:240-259): returns (batch, obs [B, N, D] host float32)."""
     seeds = list(seeds)
     if not seeds:

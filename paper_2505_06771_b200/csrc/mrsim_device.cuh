@@ -101,7 +101,10 @@ struct Rng {  // SplitRng{key, ctr} (rng.hpp:25-67)
     __device__ __forceinline__ double uniform() {  // rng.hpp:45-47
         return static_cast<double>(next_u64() >> 11) * 0x1.0p-53;
     }
-    __device__ __forceinline__ double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+    // lo + (hi - lo) * u with the reference's two roundings (no FMA contraction)
+    __device__ __forceinline__ double uniform(double lo, double hi) {
+        return __dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), uniform()));
+    }
     __device__ __forceinline__ uint64_t uniform_int(uint64_t n) {  // rng.hpp:52-55 (128-bit mulhi)
         return __umul64hi(next_u64(), n);
     }

@@ -83,7 +83,7 @@ __device__ inline int sample_poses_dev(int n, double xmin, double xmax, double y
         for (int attempt = 0; attempt < 1000 && !placed; ++attempt) {
             const double px = rng.uniform(xmin, xmax);
             const double py = rng.uniform(ymin, ymax);
-            const double pt = 3.14159265358979323846 * (1.0 - 2.0 * rng.uniform());
+            const double pt = __dmul_rn(3.14159265358979323846, __dsub_rn(1.0, __dmul_rn(2.0, rng.uniform())));
             bool ok = true;
             for (int q = 0; q < i; ++q)
                 if (hypot(px - o.x[q], py - o.y[q]) < min_sep) { ok = false; break; }
@@ -200,9 +200,9 @@ __device__ inline int reset_task(const mrsim_cfg& c, uint64_t key, ResetOut& o, 
         o.ti[0] = 0;
     } else if (TASK == MRSIM_TASK_MATERIAL_TRANSPORT) {  // material_transport.hpp:28-40
         // normal(mean, sd) = mean + sd * normal() (rng.hpp:66)
-        const double cn = y.mt_circle_mean + sqrt(y.mt_circle_variance) * rng.normal();
+        const double cn = __dadd_rn(y.mt_circle_mean, __dmul_rn(sqrt(y.mt_circle_variance), rng.normal()));
         const double circle = fmax(0.0, round(cn));
-        const double rn = y.mt_rect_mean + sqrt(y.mt_rect_variance) * rng.normal();
+        const double rn = __dadd_rn(y.mt_rect_mean, __dmul_rn(sqrt(y.mt_rect_variance), rng.normal()));
         const double rect = fmax(0.0, round(rn));
         o.tf[0] = circle;
         o.tf[1] = rect;
@@ -288,8 +288,8 @@ __device__ Real transition_task(const mrsim_cfg& c, EnvView<Real>& v, Rng& rng, 
             Real cx = px, cy = py;
             if (k > 0) {
                 const double ang = (k - 1) * (3.14159265358979323846 / 4.0);
-                cx = px + Real(cos(ang) * prey_step);
-                cy = py + Real(sin(ang) * prey_step);
+                cx = px + Real(__dmul_rn(cos(ang), prey_step));
+                cy = py + Real(__dmul_rn(sin(ang), prey_step));
             }
             if (!(cx >= -hw && cx <= hw && cy >= -hh && cy <= hh)) continue;
             Real nearest = Consts<Real>::inf;

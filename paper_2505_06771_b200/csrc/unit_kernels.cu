@@ -156,6 +156,22 @@ __global__ void __launch_bounds__(256) barrier_batch_kernel(const __grid_constan
     }
 }
 
+// FMA-chain probe: 8 independent chains per thread, ITERS iterations.
+template <class Real>
+__global__ void __launch_bounds__(256) fma_probe_kernel(Real* out, int iters, Real a, Real b) {
+    Real x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = Real(threadIdx.x + k) * Real(1e-3);
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = fma(x[k], a, b);
+    }
+    Real s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += x[k];
+    if (s == Real(12345.678)) out[0] = s;  // keep the chains live
+}
+
 }  // namespace mrsim_dev
 
 namespace {
@@ -192,6 +208,37 @@ cudaError_t run_barrier(const mrsim_cfg& c, int count, const double* dp, const d
 }  // namespace
 
 extern "C" {
+
+double mrsim_probe_fma_peak(int device, int fp64) {
+    if (cudaSetDevice(device) != cudaSuccess) return -1.0;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    void* out = nullptr;
+    cudaMalloc(&out, 16);
+    const int iters = 1 << 14, block = 256, grid = sms * 8;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int rep = 0; rep < 4; ++rep) {
+        cudaEventRecord(e0);
+        if (fp64)
+            mrsim_dev::fma_probe_kernel<double><<<grid, block>>>(static_cast<double*>(out), iters, 0.999999, 1e-7);
+        else
+            mrsim_dev::fma_probe_kernel<float><<<grid, block>>>(static_cast<float*>(out), iters, 0.999999f, 1e-7f);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (rep > 0 && ms < best) best = ms;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    if (cudaGetLastError() != cudaSuccess) return -1.0;
+    const double flops = 2.0 * 8.0 * iters * static_cast<double>(grid) * block;
+    return flops / (best * 1e-3);
+}
 
 int mrsim_qp_solve_batch(int device, int fp64, int count, int n, int m, const double* A, const double* b,
                          const double* lo, const double* hi, const double* u_nom, double tolerance, double* u_out,
