@@ -19,7 +19,7 @@ build/obj/%.o: $(PKG)/csrc/%.cu $(HDR)
 	@mkdir -p build/obj
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-oracle:
+oracle: $(LIB)
 	$(MAKE) -C oracle all
 
 clean:

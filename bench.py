@@ -249,7 +249,7 @@ def main():
         if dist:
             dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
         h2d = B * a.robots  # int8 actions
-        d2h = B * a.robots * cfg.obs_dim * 4 + B * 4 + B
+        d2h = B * a.robots * cfg.obs_dim * 4 + B * 8 + B
         e2e = {"value": world * B * a.e2e_steps / float(t_e2e.item()), "unit": "env-steps/s",
                "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
                "api": "mrsim_step_host (host buffers, synchronous)"}

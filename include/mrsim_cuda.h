@@ -275,7 +275,12 @@ int mrsim_step(mrsim_ctx* ctx, const int8_t* actions_dev, float* obs_dev, float*
  * Transactional: on error the batch state is left as before the call
  * (step_batch is pure, batch.hpp:267). Any output pointer may be NULL. */
 int mrsim_step_host(mrsim_ctx* ctx, const int32_t* actions_host, float* obs_host,
-                    float* reward_host, uint8_t* done_host, void* stream);
+                    double* reward_host, uint8_t* done_host, void* stream);
+/* assemble_observations (batch.hpp:143-151) of the current state of every
+ * env, on the device (obs_dev [num_envs][N][D] fp32, stream-ordered) or into
+ * a host buffer (synchronous). */
+int mrsim_observe(mrsim_ctx* ctx, float* obs_dev, void* stream);
+int mrsim_observe_host(mrsim_ctx* ctx, float* obs_host);
 /* Draw the harness random-policy actions for the current step into actions_dev. */
 int mrsim_random_actions(mrsim_ctx* ctx, int8_t* actions_dev, void* stream);
 /* Wait for the context's work on `stream` and report sticky device errors. */

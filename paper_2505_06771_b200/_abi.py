@@ -98,8 +98,10 @@ FUNCTIONS = {
     "mrsim_reset_episodes": (ctypes.c_int, [c_void_p, ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64,
                                             c_void_p, c_void_p]),
     "mrsim_step": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
-    "mrsim_step_host": (ctypes.c_int, [c_void_p, P(ctypes.c_int32), P(ctypes.c_float), P(ctypes.c_float),
+    "mrsim_step_host": (ctypes.c_int, [c_void_p, P(ctypes.c_int32), P(ctypes.c_float), P(ctypes.c_double),
                                        P(ctypes.c_uint8), c_void_p]),
+    "mrsim_observe": (ctypes.c_int, [c_void_p, c_void_p, c_void_p]),
+    "mrsim_observe_host": (ctypes.c_int, [c_void_p, P(ctypes.c_float)]),
     "mrsim_random_actions": (ctypes.c_int, [c_void_p, c_void_p, c_void_p]),
     "mrsim_sync": (ctypes.c_int, [c_void_p, c_void_p]),
     "mrsim_get_env_states": (ctypes.c_int, [c_void_p, ctypes.c_int64, ctypes.c_int64, P(EnvState)]),

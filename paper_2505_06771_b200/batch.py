@@ -209,13 +209,19 @@ class CudaEnvBatch:
         """Synchronous step with host buffers (the reference's std::vector<int> actions)."""
         a = np.ascontiguousarray(np.asarray(actions, dtype=np.int32).reshape(self.num_envs, self.N))
         obs = np.empty((self.num_envs, self.N, self.D), dtype=np.float32)
-        rew = np.empty((self.num_envs,), dtype=np.float32)
+        rew = np.empty((self.num_envs,), dtype=np.float64)
         done = np.empty((self.num_envs,), dtype=np.uint8)
         self._check(lib().mrsim_step_host(
             self._h, a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
-            obs.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), rew.ctypes.data_as(ctypes.POINTER(ctypes.c_float)),
+            obs.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), rew.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
             done.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), _stream_handle(None)))
         return obs, rew, done
+
+    def observe(self):
+        """assemble_observations of the current state (host float32 [B, N, D])."""
+        obs = np.empty((self.num_envs, self.N, self.D), dtype=np.float32)
+        self._check(lib().mrsim_observe_host(self._h, obs.ctypes.data_as(ctypes.POINTER(ctypes.c_float))))
+        return obs
 
     def random_actions(self, stream=None):
         self._check(lib().mrsim_random_actions(self._h, ctypes.c_void_p(self._actions.data_ptr()),

@@ -46,7 +46,7 @@ struct mrsim_ctx {
     // host-API scratch
     int8_t* d_actions = nullptr;
     float* d_obs = nullptr;
-    float* d_reward = nullptr;
+    double* d_reward64 = nullptr;
     uint8_t* d_done = nullptr;
     int8_t* h_actions = nullptr;  // pinned
     bool reset_done = false;
@@ -155,6 +155,24 @@ cudaError_t dispatch_reset(int task, const ResetParams<Real>& p, cudaStream_t s)
     }
 }
 
+template <class Real>
+cudaError_t dispatch_observe(mrsim_ctx* ctx, const DevState<Real>& s, float* obs, cudaStream_t st) {
+    using namespace mrsim_host;
+    const mrsim_cfg& c = ctx->cfg;
+    const int a = ctx->L, D = ctx->D, bd = ctx->bdim, nf = ctx->nf, ni = ctx->ni, sg = ctx->smem_group;
+    const long long B = ctx->B;
+    switch (c.task) {
+        case 0: return launch_observe<Real, 0>(c, s, obs, B, a, D, bd, nf, ni, sg, st);
+        case 1: return launch_observe<Real, 1>(c, s, obs, B, a, D, bd, nf, ni, sg, st);
+        case 2: return launch_observe<Real, 2>(c, s, obs, B, a, D, bd, nf, ni, sg, st);
+        case 3: return launch_observe<Real, 3>(c, s, obs, B, a, D, bd, nf, ni, sg, st);
+        case 4: return launch_observe<Real, 4>(c, s, obs, B, a, D, bd, nf, ni, sg, st);
+        case 5: return launch_observe<Real, 5>(c, s, obs, B, a, D, bd, nf, ni, sg, st);
+        case 6: return launch_observe<Real, 6>(c, s, obs, B, a, D, bd, nf, ni, sg, st);
+        default: return launch_observe<Real, 7>(c, s, obs, B, a, D, bd, nf, ni, sg, st);
+    }
+}
+
 const char* err_text(unsigned code) {
     switch (code) {
         case mrsim_dev::kErrInvalidAction: return "step_batch: invalid action";
@@ -207,7 +225,7 @@ int check_device_error(mrsim_ctx* ctx, bool rollback) {
 
 template <class Real>
 int do_step(mrsim_ctx* ctx, DevState<Real>* s, const int8_t* actions, float* obs, float* reward, uint8_t* done,
-            float* next_obs, cudaStream_t stream) {
+            float* next_obs, cudaStream_t stream, double* reward64 = nullptr) {
     StepParams<Real> p;
     std::memset(&p, 0, sizeof p);
     p.c = ctx->cfg;
@@ -217,6 +235,7 @@ int do_step(mrsim_ctx* ctx, DevState<Real>* s, const int8_t* actions, float* obs
     p.actions = actions;
     p.obs = obs;
     p.reward = reward;
+    p.reward64 = reward64;
     p.done = done;
     p.next_obs = next_obs;
     p.err = ctx->d_err;
@@ -586,7 +605,7 @@ void mrsim_destroy(mrsim_ctx* ctx) {
     cudaFree(ctx->d_err);
     cudaFree(ctx->d_actions);
     cudaFree(ctx->d_obs);
-    cudaFree(ctx->d_reward);
+    cudaFree(ctx->d_reward64);
     cudaFree(ctx->d_done);
     if (ctx->h_actions) cudaFreeHost(ctx->h_actions);
     delete ctx;
@@ -646,20 +665,19 @@ int mrsim_sync(mrsim_ctx* ctx, void* stream) {
     return check_device_error(ctx, true);
 }
 
-int mrsim_step_host(mrsim_ctx* ctx, const int32_t* actions_host, float* obs_host, float* reward_host,
+int mrsim_step_host(mrsim_ctx* ctx, const int32_t* actions_host, float* obs_host, double* reward_host,
                     uint8_t* done_host, void* stream) {
     if (!ctx || !actions_host) return MRSIM_E_INVALID_ARGUMENT;
+    if (!ctx->reset_done) return set_err(ctx, MRSIM_E_INVALID_ARGUMENT, "step before reset");
     CK(cudaSetDevice(ctx->device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const long long BN = ctx->B * ctx->N;
     const size_t obs_bytes = sizeof(float) * BN * ctx->D;
-    if (!ctx->d_actions) {
-        CK(cudaMalloc(&ctx->d_actions, BN));
-        CK(cudaMalloc(&ctx->d_obs, obs_bytes));
-        CK(cudaMalloc(&ctx->d_reward, 4 * ctx->B));
-        CK(cudaMalloc(&ctx->d_done, ctx->B));
-        CK(cudaMallocHost(&ctx->h_actions, BN));
-    }
+    if (!ctx->d_actions) CK(cudaMalloc(&ctx->d_actions, BN));
+    if (!ctx->d_obs) CK(cudaMalloc(&ctx->d_obs, obs_bytes));
+    if (!ctx->d_reward64) CK(cudaMalloc(&ctx->d_reward64, 8 * ctx->B));
+    if (!ctx->d_done) CK(cudaMalloc(&ctx->d_done, ctx->B));
+    if (!ctx->h_actions) CK(cudaMallocHost(&ctx->h_actions, BN));
     // validate_actions (batch.hpp:226-237): sequential, first offender reported
     for (long long k = 0; k < BN; ++k) {
         const int a = actions_host[k];
@@ -672,13 +690,38 @@ int mrsim_step_host(mrsim_ctx* ctx, const int32_t* actions_host, float* obs_host
         ctx->h_actions[k] = static_cast<int8_t>(a);
     }
     CK(cudaMemcpyAsync(ctx->d_actions, ctx->h_actions, BN, cudaMemcpyHostToDevice, s));
-    int rc = mrsim_step(ctx, ctx->d_actions, obs_host ? ctx->d_obs : nullptr, reward_host ? ctx->d_reward : nullptr,
-                        done_host ? ctx->d_done : nullptr, nullptr, stream);
+    int rc = ctx->fp64 ? do_step<double>(ctx, ctx->sd, ctx->d_actions, obs_host ? ctx->d_obs : nullptr, nullptr,
+                                         done_host ? ctx->d_done : nullptr, nullptr, s,
+                                         reward_host ? ctx->d_reward64 : nullptr)
+                       : do_step<float>(ctx, ctx->sf, ctx->d_actions, obs_host ? ctx->d_obs : nullptr, nullptr,
+                                        done_host ? ctx->d_done : nullptr, nullptr, s,
+                                        reward_host ? ctx->d_reward64 : nullptr);
     if (rc != MRSIM_OK) return rc;
     if (obs_host) CK(cudaMemcpyAsync(obs_host, ctx->d_obs, obs_bytes, cudaMemcpyDeviceToHost, s));
-    if (reward_host) CK(cudaMemcpyAsync(reward_host, ctx->d_reward, 4 * ctx->B, cudaMemcpyDeviceToHost, s));
+    if (reward_host) CK(cudaMemcpyAsync(reward_host, ctx->d_reward64, 8 * ctx->B, cudaMemcpyDeviceToHost, s));
     if (done_host) CK(cudaMemcpyAsync(done_host, ctx->d_done, ctx->B, cudaMemcpyDeviceToHost, s));
     return mrsim_sync(ctx, stream);
+}
+
+int mrsim_observe(mrsim_ctx* ctx, float* obs_dev, void* stream) {
+    if (!ctx || !obs_dev) return MRSIM_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e = ctx->fp64 ? dispatch_observe<double>(ctx, ctx->sd[ctx->cur], obs_dev, s)
+                              : dispatch_observe<float>(ctx, ctx->sf[ctx->cur], obs_dev, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "observe kernel launch");
+    return MRSIM_OK;
+}
+
+int mrsim_observe_host(mrsim_ctx* ctx, float* obs_host) {
+    if (!ctx || !obs_host) return MRSIM_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(ctx->device));
+    const size_t obs_bytes = sizeof(float) * ctx->B * ctx->N * ctx->D;
+    if (!ctx->d_obs) CK(cudaMalloc(&ctx->d_obs, obs_bytes));
+    int rc = mrsim_observe(ctx, ctx->d_obs, nullptr);
+    if (rc != MRSIM_OK) return rc;
+    CK(cudaMemcpy(obs_host, ctx->d_obs, obs_bytes, cudaMemcpyDeviceToHost));
+    return MRSIM_OK;
 }
 
 int mrsim_random_actions(mrsim_ctx* ctx, int8_t* actions_dev, void* stream) {

@@ -40,6 +40,9 @@ cudaError_t launch_step(const mrsim_dev::StepParams<Real>& p, int L, int grid, i
 template <class Real, int TASK>
 cudaError_t step_occupancy(int L, int block, int smem, int* blocks_per_sm);
 template <class Real, int TASK>
+cudaError_t launch_observe(const mrsim_cfg& c, const mrsim_dev::DevState<Real>& s, float* obs, long long B, int L,
+                           int D, int bdim, int nf, int ni, int smem_group, cudaStream_t stream);
+template <class Real, int TASK>
 cudaError_t launch_reset(const mrsim_dev::ResetParams<Real>& p, cudaStream_t stream);
 
 }  // namespace mrsim_host

@@ -55,6 +55,33 @@ cudaError_t step_occupancy<double, MRSIM_TASK_ID>(int L, int block, int smem, in
     if (L == 16) return occ_L<double, 16>(block, smem, bps);
     return occ_L<double, 32>(block, smem, bps);
 }
+template <class Real, int L>
+static cudaError_t observe_L(const mrsim_cfg& c, const mrsim_dev::DevState<Real>& s, float* obs, long long B, int D,
+                             int bdim, int nf, int ni, int smem_group, cudaStream_t st) {
+    const int block = 256, gpb = block / L;
+    const unsigned grid = static_cast<unsigned>((B + gpb - 1) / gpb);
+    auto k = mrsim_dev::observe_kernel<Real, L, MRSIM_TASK_ID>;
+    if (smem_group * gpb > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_group * gpb);
+    k<<<grid, block, smem_group * gpb, st>>>(c, s, obs, B, c.num_robots, D, bdim, nf, ni, smem_group);
+    return cudaGetLastError();
+}
+template <>
+cudaError_t launch_observe<float, MRSIM_TASK_ID>(const mrsim_cfg& c, const mrsim_dev::DevState<float>& s, float* obs,
+                                                 long long B, int L, int D, int bdim, int nf, int ni, int sg,
+                                                 cudaStream_t st) {
+    if (L == 8) return observe_L<float, 8>(c, s, obs, B, D, bdim, nf, ni, sg, st);
+    if (L == 16) return observe_L<float, 16>(c, s, obs, B, D, bdim, nf, ni, sg, st);
+    return observe_L<float, 32>(c, s, obs, B, D, bdim, nf, ni, sg, st);
+}
+template <>
+cudaError_t launch_observe<double, MRSIM_TASK_ID>(const mrsim_cfg& c, const mrsim_dev::DevState<double>& s,
+                                                  float* obs, long long B, int L, int D, int bdim, int nf, int ni,
+                                                  int sg, cudaStream_t st) {
+    if (L == 8) return observe_L<double, 8>(c, s, obs, B, D, bdim, nf, ni, sg, st);
+    if (L == 16) return observe_L<double, 16>(c, s, obs, B, D, bdim, nf, ni, sg, st);
+    return observe_L<double, 32>(c, s, obs, B, D, bdim, nf, ni, sg, st);
+}
+
 template <>
 cudaError_t launch_reset<float, MRSIM_TASK_ID>(const mrsim_dev::ResetParams<float>& p, cudaStream_t s) {
     const int block = 128;

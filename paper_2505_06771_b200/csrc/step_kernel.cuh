@@ -58,6 +58,7 @@ struct StepParams {
     const int8_t* actions;  // [B][N] or nullptr (on-device random policy)
     float* obs;             // [B][N][D] or nullptr
     float* reward;          // [B] or nullptr
+    double* reward64;       // [B] or nullptr (host-API path: the reference's double team reward)
     uint8_t* done;          // [B] or nullptr
     float* next_obs;        // [B][N][D] or nullptr
     unsigned long long* err;
@@ -564,6 +565,7 @@ __global__ void __launch_bounds__(256) step_kernel(const __grid_constant__ StepP
             if (done) finalize_task<TASK, Real>(c, v, metric, success);
             ep_return += reward;
             if (p.reward) p.reward[e] = static_cast<float>(reward);
+            if (p.reward64) p.reward64[e] = static_cast<double>(reward);
             if (p.done) p.done[e] = static_cast<uint8_t>(done);
             if (done && new_step == c.max_steps) {  // EpisodeStats (harness.hpp:277-285)
                 p.st.episodes[e] += 1;
@@ -722,6 +724,34 @@ __global__ void __launch_bounds__(128) reset_kernel(const __grid_constant__ Rese
         float* o = p.obs + e * N * p.D;
         for (int r = 0; r < N; ++r)
             for (int q = 0; q < p.D; ++q) o[r * p.D + q] = obs_feature<TASK, Real>(c, v, r, q, p.bdim);
+    }
+}
+
+// assemble_observations of the current state (batch.hpp:143-151), one group per env.
+template <class Real, int L, int TASK>
+__global__ void __launch_bounds__(256) observe_kernel(const __grid_constant__ mrsim_cfg c, DevState<Real> s, float* obs,
+                                                      long long B, int N, int D, int bdim, int nf, int ni,
+                                                      int smem_bytes_per_group) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const Group<L> g;
+    const int gib = threadIdx.x / L;
+    const long long e = static_cast<long long>(blockIdx.x) * (blockDim.x / L) + gib;
+    if (e >= B) return;
+    GroupSmem<Real> sm;
+    sm.carve(smem_raw + gib * smem_bytes_per_group, 2 * N, N);
+    for (int i = g.lane; i < N; i += L) {
+        sm.xs[i] = s.px[e * N + i];
+        sm.ys[i] = s.py[e * N + i];
+        sm.ts[i] = s.pt[e * N + i];
+    }
+    for (int f = g.lane; f < nf; f += L) sm.tf[f] = s.tf[static_cast<long long>(f) * B + e];
+    for (int w = g.lane; w < ni; w += L) sm.ti[w] = s.ti[static_cast<long long>(w) * B + e];
+    g.sync();
+    const EnvView<Real> view{sm.xs, sm.ys, sm.ts, sm.tf, sm.ti, N};
+    float* o = obs + e * N * D;
+    for (int q = g.lane; q < N * D; q += L) {
+        const int r = q / D;
+        o[q] = obs_feature<TASK, Real>(c, view, r, q - r * D, bdim);
     }
 }
 
