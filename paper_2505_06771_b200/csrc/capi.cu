@@ -40,7 +40,7 @@ struct mrsim_ctx {
     long long env_steps = 0;
     std::string last_error;
     int num_sms = 148;
-    int block = 256;
+    int block = 128;
     int grid = 0;
     int smem_group = 0;
     // host-API scratch
@@ -159,17 +159,17 @@ template <class Real>
 cudaError_t dispatch_observe(mrsim_ctx* ctx, const DevState<Real>& s, float* obs, cudaStream_t st) {
     using namespace mrsim_host;
     const mrsim_cfg& c = ctx->cfg;
-    const int a = ctx->L, D = ctx->D, bd = ctx->bdim, nf = ctx->nf, ni = ctx->ni, sg = ctx->smem_group;
+    const int D = ctx->D, bd = ctx->bdim, nf = ctx->nf, ni = ctx->ni;
     const long long B = ctx->B;
     switch (c.task) {
-        case 0: return launch_observe<Real, 0>(c, s, obs, B, a, D, bd, nf, ni, sg, st);
-        case 1: return launch_observe<Real, 1>(c, s, obs, B, a, D, bd, nf, ni, sg, st);
-        case 2: return launch_observe<Real, 2>(c, s, obs, B, a, D, bd, nf, ni, sg, st);
-        case 3: return launch_observe<Real, 3>(c, s, obs, B, a, D, bd, nf, ni, sg, st);
-        case 4: return launch_observe<Real, 4>(c, s, obs, B, a, D, bd, nf, ni, sg, st);
-        case 5: return launch_observe<Real, 5>(c, s, obs, B, a, D, bd, nf, ni, sg, st);
-        case 6: return launch_observe<Real, 6>(c, s, obs, B, a, D, bd, nf, ni, sg, st);
-        default: return launch_observe<Real, 7>(c, s, obs, B, a, D, bd, nf, ni, sg, st);
+        case 0: return launch_observe<Real, 0>(c, s, obs, B, D, bd, nf, ni, st);
+        case 1: return launch_observe<Real, 1>(c, s, obs, B, D, bd, nf, ni, st);
+        case 2: return launch_observe<Real, 2>(c, s, obs, B, D, bd, nf, ni, st);
+        case 3: return launch_observe<Real, 3>(c, s, obs, B, D, bd, nf, ni, st);
+        case 4: return launch_observe<Real, 4>(c, s, obs, B, D, bd, nf, ni, st);
+        case 5: return launch_observe<Real, 5>(c, s, obs, B, D, bd, nf, ni, st);
+        case 6: return launch_observe<Real, 6>(c, s, obs, B, D, bd, nf, ni, st);
+        default: return launch_observe<Real, 7>(c, s, obs, B, D, bd, nf, ni, st);
     }
 }
 
@@ -530,7 +530,7 @@ int mrsim_create(const mrsim_cfg* cfg, int device, int64_t num_envs, uint32_t fl
     ctx->D = mrsim_dev::obs_dim_of(*cfg);
     ctx->bdim = mrsim_dev::base_obs_dim(*cfg);
     mrsim_dev::task_fields(*cfg, &ctx->nf, &ctx->ni);
-    ctx->L = ctx->n <= 8 ? 8 : (ctx->n <= 16 ? 16 : 32);
+    ctx->L = ctx->N <= 4 ? 4 : (ctx->N <= 8 ? 8 : 16);  // lane per robot
     cudaError_t e = cudaSetDevice(device);
     if (e != cudaSuccess) {
         rc = cuda_fail(ctx, e, "cudaSetDevice");
@@ -580,8 +580,8 @@ int mrsim_create(const mrsim_cfg* cfg, int device, int64_t num_envs, uint32_t fl
     cudaMemcpy(ctx->d_err, &none, sizeof none, cudaMemcpyHostToDevice);
     cudaMemset(ctx->d_err_serial, 0xff, 8);
     // launch geometry: persistent grid of (SMs x resident blocks)
-    ctx->smem_group = ctx->fp64 ? mrsim_dev::GroupSmem<double>::bytes(ctx->n, ctx->N)
-                                : mrsim_dev::GroupSmem<float>::bytes(ctx->n, ctx->N);
+    ctx->smem_group = ctx->fp64 ? mrsim_dev::GroupSmem<double>::bytes(ctx->N, ctx->nf, ctx->ni)
+                                : mrsim_dev::GroupSmem<float>::bytes(ctx->N, ctx->nf, ctx->ni);
     const int smem = ctx->smem_group * (ctx->block / ctx->L);
     int bps = 0;
     e = ctx->fp64 ? dispatch_occ<double>(cfg->task, ctx->L, ctx->block, smem, &bps)

@@ -20,6 +20,7 @@ inline void fill_consts(const mrsim_cfg& c, mrsim_dev::PhysConsts<Real>& k) {
     k.coll_r = Real(c.collision_radius);
     k.k_pos = Real(c.k_position);
     k.l = Real(l);
+    k.inv_l = Real(1.0 / l);
     k.gamma = Real(c.barrier_gain);
     const double r_eff = c.safety_radius + 2.0 * l + c.discrete_margin;  // barrier.hpp:155
     k.r_eff2 = Real(r_eff * r_eff);
@@ -40,8 +41,8 @@ cudaError_t launch_step(const mrsim_dev::StepParams<Real>& p, int L, int grid, i
 template <class Real, int TASK>
 cudaError_t step_occupancy(int L, int block, int smem, int* blocks_per_sm);
 template <class Real, int TASK>
-cudaError_t launch_observe(const mrsim_cfg& c, const mrsim_dev::DevState<Real>& s, float* obs, long long B, int L,
-                           int D, int bdim, int nf, int ni, int smem_group, cudaStream_t stream);
+cudaError_t launch_observe(const mrsim_cfg& c, const mrsim_dev::DevState<Real>& s, float* obs, long long B, int D,
+                           int bdim, int nf, int ni, cudaStream_t stream);
 template <class Real, int TASK>
 cudaError_t launch_reset(const mrsim_dev::ResetParams<Real>& p, cudaStream_t stream);
 

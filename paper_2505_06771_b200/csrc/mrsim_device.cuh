@@ -127,76 +127,6 @@ __host__ __device__ __forceinline__ uint64_t policy_key_of(uint64_t seed) {
 }
 
 // ---------------------------------------------------------------------------
-// Sub-warp group of L lanes cooperating on one environment.
-// ---------------------------------------------------------------------------
-template <int L>
-struct Group {
-    static_assert(L == 8 || L == 16 || L == 32, "group size");
-    unsigned mask;
-    int lane;  // 0..L-1
-    __device__ __forceinline__ Group() {
-        const int wl = threadIdx.x & 31;
-        lane = wl & (L - 1);
-        mask = (L == 32) ? 0xffffffffu : (((1u << L) - 1u) << (wl & ~(L - 1)));
-    }
-    __device__ __forceinline__ void sync() const { __syncwarp(mask); }
-    template <class T>
-    __device__ __forceinline__ T shfl(T v, int src) const { return __shfl_sync(mask, v, src, L); }
-    template <class T>
-    __device__ __forceinline__ T sum(T v) const {
-#pragma unroll
-        for (int o = L / 2; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o, L);
-        return v;
-    }
-    template <class T>
-    __device__ __forceinline__ T min(T v) const {
-#pragma unroll
-        for (int o = L / 2; o > 0; o >>= 1) {
-            T w = __shfl_xor_sync(mask, v, o, L);
-            v = w < v ? w : v;
-        }
-        return v;
-    }
-    template <class T>
-    __device__ __forceinline__ T max(T v) const {
-#pragma unroll
-        for (int o = L / 2; o > 0; o >>= 1) {
-            T w = __shfl_xor_sync(mask, v, o, L);
-            v = w > v ? w : v;
-        }
-        return v;
-    }
-    __device__ __forceinline__ bool any(bool p) const { return (__ballot_sync(mask, p) & mask) != 0u; }
-    __device__ __forceinline__ unsigned ballot(bool p) const {
-        const unsigned b = __ballot_sync(mask, p) & mask;
-        return (L == 32) ? b : (b >> ((threadIdx.x & 31) & ~(L - 1)));
-    }
-    // argmax with ties to the lowest index (first-maximal semantics of the
-    // reference's `v > worst` scans, qp.hpp:228-238). idx < 0 means "none".
-    template <class T>
-    __device__ __forceinline__ void argmax(T& v, int& idx) const {
-#pragma unroll
-        for (int o = L / 2; o > 0; o >>= 1) {
-            T ov = __shfl_xor_sync(mask, v, o, L);
-            int oi = __shfl_xor_sync(mask, idx, o, L);
-            const bool take = (oi >= 0) && (idx < 0 || ov > v || (ov == v && oi < idx));
-            if (take) { v = ov; idx = oi; }
-        }
-    }
-    // argmin with ties to the lowest index (`t < t1`, qp.hpp:294-302).
-    template <class T>
-    __device__ __forceinline__ void argmin(T& v, int& idx) const {
-#pragma unroll
-        for (int o = L / 2; o > 0; o >>= 1) {
-            T ov = __shfl_xor_sync(mask, v, o, L);
-            int oi = __shfl_xor_sync(mask, idx, o, L);
-            const bool take = (oi >= 0) && (idx < 0 || ov < v || (ov == v && oi < idx));
-            if (take) { v = ov; idx = oi; }
-        }
-    }
-};
-
-// ---------------------------------------------------------------------------
 // Device error word: the first (lowest env) error wins, mirroring the
 // reference's sequential validation order (batch.hpp:226-237).
 // code layout: [env:40][robot:8][code:8] in a u64 for atomicMin.

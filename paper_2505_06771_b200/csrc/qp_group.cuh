@@ -1,5 +1,5 @@
 // qp_group.cuh — the CBF safety QP, solved cooperatively by the L lanes of
-// one environment group.
+// one environment group, in warp lockstep (see group.cuh).
 //
 //   minimize 0.5 ||u - u_nom||^2   s.t.  g_r . u <= h_r   (unit-norm rows)
 //
@@ -14,268 +14,341 @@
 //     matrix N^T N at every inner step (qp.hpp:199-221). Adding a row is one
 //     Gram-Schmidt column (the residual z the step needs anyway), dropping
 //     a row is k Givens rotations; r = (N^T N)^{-1} N^T g = R^{-1} Q^T g.
-//   * lane v owns variable v (u_v, g_v, z_v); lane a owns active slot a
-//     (c_a, r_a, lambda_a). Reductions are butterfly shuffles in the group.
-//   * rows are never materialised in HBM: the RowSet policy evaluates them
-//     on the fly (barrier rows from the robots' projected points, or dense
-//     rows for the unit-level entry point).
+//   * lane l owns variables 2l, 2l+1 (one robot: u_x, u_y) and active slots
+//     l, l+L, ...; reductions are shuffles over the group's lanes.
+//   * every loop that contains a collective has a warp-uniform trip count;
+//     per-environment decisions are predicates, so the whole warp (32/L
+//     environments) runs in lockstep with full-mask shuffles.
+//   * rows are never materialised: the RowSet policy evaluates them on the
+//     fly (barrier rows from the robots' projected points, or dense rows
+//     for the unit-level entry point).
 #pragma once
 
+#include "group.cuh"
 #include "mrsim_device.cuh"
 
 namespace mrsim_dev {
 
 enum QpStatusDev : int { kQpOptimal = 0, kQpInfeasible = 1, kQpIterLimit = 2 };
 
-// Shared-memory workspace of one group for n <= L variables.
-//   Q: column a (active slot a) at Q + a*(n+1), indexed by variable
-//   R: R[row][col] at R + col*(n+1) + row (upper triangular)
-//   gp, c: broadcast scratch [n]; act: active row indices [n]
+// Shared-memory workspace of one group for n variables:
+//   Q[a*n + v] (column a = active slot a), R[col*n + row] (upper triangular),
+//   gS (entering normal), cS (Q^T g), rS (R^{-1} c), lamS (multipliers), act (row ids)
 template <class Real>
-struct QpSmem {
-    Real* Q;
-    Real* R;
-    Real* gp;
-    Real* c;
+struct QpWs {
+    Real *Q, *R, *gS, *cS, *rS, *lamS;
     int* act;
-    static __host__ __device__ constexpr int reals(int n) { return 2 * n * (n + 1) + 2 * n; }
+    static __host__ __device__ constexpr int reals(int n) { return 2 * n * n + 4 * n; }
     static __host__ __device__ constexpr int ints(int n) { return n; }
     __device__ void carve(Real* base, int* ibase, int n) {
         Q = base;
-        R = Q + n * (n + 1);
-        gp = R + n * (n + 1);
-        c = gp + n;
+        R = Q + n * n;
+        gS = R + n * n;
+        cS = gS + n;
+        rS = cS + n;
+        lamS = rS + n;
         act = ibase;
     }
 };
 
-// Drop active slot b: delete column b of N = Q R and restore triangularity
-// with Givens rotations (the reference erases active[b] / lambda[b] and
-// re-factorises, qp.hpp:270-271, 312-313, 327-328; order is preserved).
+// Drop active slot `bi` of the groups with do_drop set (the reference erases
+// active[b] / lambda[b] and re-factorises, qp.hpp:270-271, 312-313, 327-328):
+// delete column bi of R and restore triangularity with Givens rotations that
+// are applied to Q's columns as well. Order of the remaining slots is kept.
 template <class Real, int L, class RowSet>
-__device__ __forceinline__ void qp_drop(const Group<L>& g, RowSet& rows, const QpSmem<Real>& ws, int n, int& k,
-                                        Real& lam, int b) {
+__device__ __forceinline__ void qp_drop(const Grp<L>& g, RowSet& rows, const QpWs<Real>& ws, int n, int& k,
+                                        bool do_drop, int bi) {
     const int lane = g.lane;
-    const int s = n + 1;
-    rows.set_active(g, ws.act[b], false);
-    // shift multipliers and active indices down over slot b
-    const Real lam_up = g.shfl(lam, lane + 1 < L ? lane + 1 : lane);
-    int act_up = (lane + 1 < k) ? ws.act[lane + 1] : 0;
-    g.sync();
-    if (lane >= b && lane < k - 1) {
-        lam = lam_up;
-        ws.act[lane] = act_up;
+    if (do_drop) rows.set_active(g, ws.act[bi], false);
+    Real tl0 = 0, tl1 = 0;
+    int ta0 = 0, ta1 = 0;
+    const int a0 = lane, a1 = lane + L;
+    const bool m0 = do_drop && a0 >= bi && a0 < k - 1;
+    const bool m1 = do_drop && a1 >= bi && a1 < k - 1;
+    if (m0) { tl0 = ws.lamS[a0 + 1]; ta0 = ws.act[a0 + 1]; }
+    if (m1) { tl1 = ws.lamS[a1 + 1]; ta1 = ws.act[a1 + 1]; }
+    Grp<L>::sync();
+    if (m0) { ws.lamS[a0] = tl0; ws.act[a0] = ta0; }
+    if (m1) { ws.lamS[a1] = tl1; ws.act[a1] = ta1; }
+    if (do_drop) {  // delete column bi of R (lane = rows lane, lane+L)
+        for (int row = lane; row < k; row += L)
+            for (int col = bi; col < k - 1; ++col) ws.R[col * n + row] = ws.R[(col + 1) * n + row];
     }
-    // delete column b of R (lane = row)
-    if (lane < k) {
-        for (int col = b; col < k - 1; ++col) ws.R[col * s + lane] = ws.R[(col + 1) * s + lane];
-    }
-    g.sync();
-    for (int j = b; j < k - 1; ++j) {
-        const Real a = ws.R[j * s + j];
-        const Real bb = ws.R[j * s + j + 1];
-        g.sync();
-        const Real rho = dhypot(a, bb);
-        const Real cg = a / rho, sg = bb / rho;
-        if (lane >= j && lane < k - 1) {  // rows j, j+1 of R, column = lane
-            const Real x = ws.R[lane * s + j], y = ws.R[lane * s + j + 1];
-            ws.R[lane * s + j] = cg * x + sg * y;
-            ws.R[lane * s + j + 1] = (lane == j) ? Real(0) : (-sg * x + cg * y);
+    Grp<L>::sync();
+    const int jmax = Grp<L>::warp_max(do_drop ? k - 1 : 0);
+    for (int j = 0; j < jmax; ++j) {
+        const bool rot = do_drop && j >= bi && j < k - 1;
+        Real a = 0, bb = 0;
+        if (rot) {
+            a = ws.R[j * n + j];
+            bb = ws.R[j * n + j + 1];
         }
-        if (lane < n) {  // columns j, j+1 of Q, row = lane
-            const Real x = ws.Q[j * s + lane], y = ws.Q[(j + 1) * s + lane];
-            ws.Q[j * s + lane] = cg * x + sg * y;
-            ws.Q[(j + 1) * s + lane] = -sg * x + cg * y;
+        Grp<L>::sync();
+        if (rot) {
+            const Real rho = dsqrt(a * a + bb * bb);
+            const Real cg = a / rho, sg = bb / rho;
+            for (int col = lane; col < k - 1; col += L) {
+                if (col < j) continue;
+                const Real x = ws.R[col * n + j], y = ws.R[col * n + j + 1];
+                ws.R[col * n + j] = cg * x + sg * y;
+                ws.R[col * n + j + 1] = (col == j) ? Real(0) : (-sg * x + cg * y);
+            }
+            if (2 * lane < n) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int v = 2 * lane + h;
+                    if (v >= n) continue;
+                    const Real x = ws.Q[j * n + v], y = ws.Q[(j + 1) * n + v];
+                    ws.Q[j * n + v] = cg * x + sg * y;
+                    ws.Q[(j + 1) * n + v] = -sg * x + cg * y;
+                }
+            }
         }
-        g.sync();
+        Grp<L>::sync();
     }
-    --k;
+    if (do_drop) --k;
 }
 
-// Solve. `u` holds u_v on lane v < n (in: u_nom, out: solution).
+// Solve for the groups with `participate` set. (ux, uy): this lane's pair of
+// variables (in: u_nom, out: solution). Returns the QpStatusDev of the group.
 template <class Real, int L, class RowSet>
-__device__ int qp_solve_group(const Group<L>& g, RowSet& rows, const QpSmem<Real>& ws, int n, Real& u,
-                              int total_rows, int max_iterations, Real tol, int* iterations_out) {
+__device__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpWs<Real>& ws, int n, bool participate, Real& ux,
+                        Real& uy, int total_rows, Real tol) {
     const int lane = g.lane;
-    const int s = n + 1;
-    int k = 0;     // active-set size (uniform across the group)
-    Real lam = 0;  // lane a < k: lambda_a
-    if (max_iterations <= 0) max_iterations = 100 + 20 * total_rows;  // qp.hpp:193
-    int iter = 0;
+    const bool vl = 2 * lane < n;      // this lane's x variable exists
+    const bool vly = 2 * lane + 1 < n;  // ... and its y variable (n may be odd for dense QPs)
+    int k = 0;
     int status = kQpOptimal;
-    for (; iter < max_iterations; ++iter) {
+    bool done = !participate;
+    int iter = 0;
+    const int max_iterations = 100 + 20 * total_rows;  // qp.hpp:193
+    while (Grp<L>::warp_any(!done)) {
+        if (!done && iter >= max_iterations) {
+            status = kQpIterLimit;
+            done = true;
+        }
         // Most violated inactive row (qp.hpp:225-239).
         Real worst = tol;
         int p = -1;
-        rows.scan(g, u, worst, p);
+        rows.scan(g, ux, uy, worst, p);
         g.argmax(worst, p);
-        if (p < 0) break;
-
-        Real gp, hp;  // lane v: component v of row p; rhs (uniform)
-        rows.fetch(g, p, gp, hp);
-        if (lane >= n) gp = 0;
+        if (!done && p < 0) done = true;
+        bool act = !done;
+        Real gx, gy, hp;
+        rows.fetch(g, act ? p : rows.dummy_row(), gx, gy, hp);
+        if (!vl) gx = Real(0);
+        if (!vly) gy = Real(0);
         // Zero-norm violated row: b < 0 on a vacuous row (qp.hpp:242-253).
-        if (g.sum(gp * gp) < Prec<Real>::eps_row) {
+        const Real gn = g.sum(gx * gx + gy * gy);
+        if (act && gn < Prec<Real>::eps_row) {
             status = kQpInfeasible;
-            break;
+            done = true;
+            act = false;
         }
-        if (lane < n) ws.gp[lane] = gp;
-        g.sync();
-
-        bool added = false;
+        if (act && vl) ws.gS[2 * lane] = gx;
+        if (act && vly) ws.gS[2 * lane + 1] = gy;
+        Grp<L>::sync();
+        bool in = act, added = false;
         Real lam_p = 0;
-        for (int guard = 0; guard <= total_rows && !added; ++guard) {  // qp.hpp:262
-            // c = Q^T g_p on lane a < k
-            Real ca = 0;
-            if (lane < k) {
-                const Real* qa = ws.Q + lane * s;
-                for (int v = 0; v < n; ++v) ca += qa[v] * ws.gp[v];
-                ws.c[lane] = ca;
+        int guard = 0;
+        while (Grp<L>::warp_any(in)) {  // qp.hpp:262-330
+            // c = Q^T g (slots of this lane), r <- c
+            if (in) {
+                for (int a = lane; a < k; a += L) {
+                    Real c = 0;
+                    for (int v = 0; v < n; ++v) c += ws.Q[a * n + v] * ws.gS[v];
+                    ws.cS[a] = c;
+                    ws.rS[a] = c;
+                }
             }
-            g.sync();
-            // z = g_p - Q c on lane v < n
-            Real z = 0;
-            if (lane < n) {
-                z = gp;
-                for (int a = 0; a < k; ++a) z -= ws.Q[a * s + lane] * ws.c[a];
+            Grp<L>::sync();
+            // z = g - Q c (this lane's two components)
+            Real zx = gx, zy = gy;
+            if (in && vl) {
+                for (int a = 0; a < k; ++a) {
+                    const Real ca = ws.cS[a];
+                    zx -= ws.Q[a * n + 2 * lane] * ca;
+                    if (vly) zy -= ws.Q[a * n + 2 * lane + 1] * ca;
+                }
             }
             // r = R^{-1} c (back substitution, column oriented)
-            Real ra = ca;
-            for (int b = k - 1; b >= 0; --b) {
-                if (lane == b) ra = ra / ws.R[b * s + b];
-                const Real rb = g.shfl(ra, b);
-                if (lane < b) ra -= ws.R[b * s + lane] * rb;
-            }
-            const Real z2 = g.sum(z * z);
-            const Real viol = g.sum(lane < n ? gp * u : Real(0)) - hp;  // qp.hpp:281
-            if (viol <= tol) {  // qp.hpp:282-289
-                if (lam_p > Real(0) && z2 > Prec<Real>::eps_z) {
-                    const Real rho = dsqrt(z2);
-                    if (lane < n) ws.Q[k * s + lane] = z / rho;
-                    if (lane < k) ws.R[k * s + lane] = ca;
-                    if (lane == k) {
-                        ws.R[k * s + k] = rho;
-                        lam = lam_p;
-                        ws.act[k] = p;
-                    }
-                    rows.set_active(g, p, true);
-                    ++k;
+            const int kmax = Grp<L>::warp_max(in ? k : 0);
+            for (int b = kmax - 1; b >= 0; --b) {
+                const bool on = in && b < k;
+                if (on && lane == (b & (L - 1))) ws.rS[b] = ws.rS[b] / ws.R[b * n + b];
+                Grp<L>::sync();
+                if (on) {
+                    const Real rb = ws.rS[b];
+                    for (int a = lane; a < b; a += L) ws.rS[a] -= ws.R[b * n + a] * rb;
                 }
-                g.sync();
-                added = true;
-                break;
+                Grp<L>::sync();
             }
+            const Real z2 = g.sum(zx * zx + zy * zy);
+            const Real viol = g.sum(gx * ux + gy * uy) - hp;  // qp.hpp:281
             // First blocking multiplier (qp.hpp:291-302).
             Real t1 = Consts<Real>::inf;
-            int blocker = -1;
-            if (lane < k && ra > Prec<Real>::eps_r) {
-                t1 = lam / ra;
-                blocker = lane;
-            }
-            g.argmin(t1, blocker);
-            if (blocker < 0) t1 = Consts<Real>::inf;
-            if (z2 <= Prec<Real>::eps_z) {  // qp.hpp:304-315
-                if (blocker < 0) {
-                    status = kQpInfeasible;
-                    if (iterations_out) *iterations_out = iter;
-                    return status;
+            int bi = -1;
+            if (in) {
+                for (int a = lane; a < k; a += L) {
+                    const Real ra = ws.rS[a];
+                    if (ra > Prec<Real>::eps_r) {
+                        const Real t = ws.lamS[a] / ra;
+                        if (bi < 0 || t < t1) {
+                            t1 = t;
+                            bi = a;
+                        }
+                    }
                 }
-                if (lane < k) lam -= t1 * ra;
-                lam_p += t1;
-                qp_drop<Real, L>(g, rows, ws, n, k, lam, blocker);
-                continue;
             }
-            const Real t2 = viol / z2;  // qp.hpp:317-329
-            const Real t = dmin(t1, t2);
-            if (lane < n) u -= t * z;
-            if (lane < k) lam -= t * ra;
-            lam_p += t;
-            if (t2 <= t1) {
+            g.argmin(t1, bi);
+            if (bi < 0) t1 = Consts<Real>::inf;
+            bool finish = false, do_add = false, do_drop = false, infeas = false, step_u = false, step_l = false;
+            Real t = 0;
+            if (in) {
+                if (viol <= tol) {  // qp.hpp:282-289
+                    finish = true;
+                    do_add = lam_p > Real(0) && z2 > Prec<Real>::eps_z;
+                } else if (z2 <= Prec<Real>::eps_z) {  // qp.hpp:304-315
+                    if (bi < 0) {
+                        infeas = true;
+                    } else {
+                        t = t1;
+                        step_l = true;
+                        do_drop = true;
+                    }
+                } else {  // qp.hpp:317-329
+                    const Real t2 = viol / z2;
+                    t = dmin(t1, t2);
+                    step_u = step_l = true;
+                    if (t2 <= t1) {
+                        do_add = true;
+                        finish = true;
+                    } else {
+                        do_drop = true;
+                    }
+                }
+            }
+            if (step_u) {
+                ux -= t * zx;
+                uy -= t * zy;
+            }
+            if (step_l) {
+                for (int a = lane; a < k; a += L) ws.lamS[a] -= t * ws.rS[a];
+                lam_p += t;
+            }
+            Grp<L>::sync();
+            if (do_add) {
                 const Real rho = dsqrt(z2);
-                if (lane < n) ws.Q[k * s + lane] = z / rho;
-                if (lane < k) ws.R[k * s + lane] = ca;
-                if (lane == k) {
-                    ws.R[k * s + k] = rho;
-                    lam = lam_p;
+                if (vl) ws.Q[k * n + 2 * lane] = zx / rho;
+                if (vly) ws.Q[k * n + 2 * lane + 1] = zy / rho;
+                for (int a = lane; a < k; a += L) ws.R[k * n + a] = ws.cS[a];
+                if (lane == 0) {
+                    ws.R[k * n + k] = rho;
+                    ws.lamS[k] = lam_p;
                     ws.act[k] = p;
                 }
                 rows.set_active(g, p, true);
                 ++k;
-                g.sync();
-                added = true;
-            } else {
-                qp_drop<Real, L>(g, rows, ws, n, k, lam, blocker);
             }
+            Grp<L>::sync();
+            qp_drop<Real, L>(g, rows, ws, n, k, do_drop, bi);
+            if (finish) {
+                in = false;
+                added = true;
+            }
+            if (infeas) {
+                in = false;
+                status = kQpInfeasible;
+                done = true;
+            }
+            ++guard;
+            if (in && guard > total_rows) in = false;  // guard exhausted without adding
         }
-        if (!added) break;  // stall (qp.hpp:331-334)
+        if (act && !added) done = true;  // stall (qp.hpp:331-334) or infeasible
+        if (act) ++iter;
     }
-    if (status == kQpOptimal && iter >= max_iterations) status = kQpIterLimit;
-    if (iterations_out) *iterations_out = iter;
     return status;
 }
 
 // ---------------------------------------------------------------------------
 // Dense rows (unit-level entry point, fold_rows qp.hpp:104-141): row r of A
 // in smem, normalised; finite box sides folded after the rows in variable
-// order, hi before lo. Owner of row r: lane r % L.
+// order, hi before lo. Row r is scanned by lane r % L; active sets are
+// group-uniform bit masks.
 // ---------------------------------------------------------------------------
 template <class Real, int L, int MAXM>
 struct DenseRows {
-    static constexpr int kSlots = (MAXM + L - 1) / L;
-    const Real* G;  // [m][n] normalised rows (smem)
-    const Real* h;  // [m]
-    Real* ush;      // [n] u broadcast scratch (smem)
-    const Real* lo;  // [n] box (global, +-1e30 = unbounded)
+    const Real* G;    // [m][n] normalised rows (smem)
+    const Real* h;    // [m]
+    Real* ush;        // [n] u broadcast scratch (smem)
+    const Real* lo;   // [n] box (+-1e30 = unbounded)
     const Real* hi;
     int n, m;
-    unsigned long long active_rows;  // bit r: row r active (uniform)
-    unsigned box_active;             // bit 2v (hi) / 2v+1 (lo) (uniform)
+    unsigned long long active_rows;  // bit r: row r active (group-uniform)
+    unsigned long long box_active;   // bit 2v (hi) / 2v+1 (lo)
 
-    __device__ void scan(const Group<L>& g, Real u, Real& worst, int& p) {
-        if (g.lane < n) ush[g.lane] = u;
-        g.sync();
-        for (int sl = 0; sl < kSlots; ++sl) {
-            const int r = g.lane + sl * L;
-            if (r < m && !((active_rows >> r) & 1ull)) {
-                Real s = 0;
-                for (int i = 0; i < n; ++i) s += G[r * n + i] * ush[i];
-                const Real v = s - h[r];
-                if (v > worst) { worst = v; p = r; }
+    __device__ int dummy_row() const { return 0; }
+
+    __device__ void scan(const Grp<L>& g, Real ux, Real uy, Real& worst, int& p) {
+        const int lane = g.lane;
+        if (2 * lane < n) ush[2 * lane] = ux;
+        if (2 * lane + 1 < n) ush[2 * lane + 1] = uy;
+        Grp<L>::sync();
+        for (int r = lane; r < m; r += L) {
+            if ((active_rows >> r) & 1ull) continue;
+            Real s = 0;
+            for (int i = 0; i < n; ++i) s += G[r * n + i] * ush[i];
+            const Real v = s - h[r];
+            if (v > worst) {
+                worst = v;
+                p = r;
             }
         }
-        if (g.lane < n) {
-            const int v = g.lane;
-            if (hi[v] < Real(1e30) && !((box_active >> (2 * v)) & 1u)) {
-                const Real val = u - hi[v];
-                if (val > worst) { worst = val; p = m + 2 * v; }
-            }
-            if (lo[v] > Real(-1e30) && !((box_active >> (2 * v + 1)) & 1u)) {
-                const Real val = -u + lo[v];
-                if (val > worst) { worst = val; p = m + 2 * v + 1; }
+        if (2 * lane < n) {
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int v = 2 * lane + c;
+                if (v >= n) continue;
+                const Real u = c ? uy : ux;
+                if (hi[v] < Real(1e30) && !((box_active >> (2 * v)) & 1ull)) {
+                    const Real val = u - hi[v];
+                    if (val > worst) { worst = val; p = m + 2 * v; }
+                }
+                if (lo[v] > Real(-1e30) && !((box_active >> (2 * v + 1)) & 1ull)) {
+                    const Real val = -u + lo[v];
+                    if (val > worst) { worst = val; p = m + 2 * v + 1; }
+                }
             }
         }
-        g.sync();
+        Grp<L>::sync();
     }
-    __device__ void fetch(const Group<L>& g, int p, Real& gv, Real& hp) const {
+    __device__ void fetch(const Grp<L>& g, int p, Real& gx, Real& gy, Real& hp) const {
+        const int lane = g.lane;
+        gx = gy = Real(0);
         if (p < m) {
-            gv = g.lane < n ? G[p * n + g.lane] : Real(0);
+            if (2 * lane < n) gx = G[p * n + 2 * lane];
+            if (2 * lane + 1 < n) gy = G[p * n + 2 * lane + 1];
             hp = h[p];
         } else {
             const int q = p - m;
             const int v = q >> 1;
             const bool is_lo = q & 1;
-            gv = (g.lane == v) ? (is_lo ? Real(-1) : Real(1)) : Real(0);
+            const Real s = is_lo ? Real(-1) : Real(1);
+            if (lane == (v >> 1)) {
+                if (v & 1) gy = s;
+                else gx = s;
+            }
             hp = is_lo ? -lo[v] : hi[v];
         }
     }
-    __device__ void set_active(const Group<L>&, int p, bool on) {
+    __device__ void set_active(const Grp<L>&, int p, bool on) {
         if (p < m) {
             if (on) active_rows |= 1ull << p;
             else active_rows &= ~(1ull << p);
         } else {
             const int q = p - m;
-            if (on) box_active |= 1u << q;
-            else box_active &= ~(1u << q);
+            if (on) box_active |= 1ull << q;
+            else box_active &= ~(1ull << q);
         }
     }
 };

@@ -32,54 +32,43 @@ static cudaError_t occ_L(int block, int smem, int* bps) {
 template <>
 cudaError_t launch_step<float, MRSIM_TASK_ID>(const mrsim_dev::StepParams<float>& p, int L, int grid, int block,
                                               int smem, cudaStream_t s) {
+    if (L == 4) return launch_L<float, 4>(p, grid, block, smem, s);
     if (L == 8) return launch_L<float, 8>(p, grid, block, smem, s);
-    if (L == 16) return launch_L<float, 16>(p, grid, block, smem, s);
-    return launch_L<float, 32>(p, grid, block, smem, s);
+    return launch_L<float, 16>(p, grid, block, smem, s);
 }
 template <>
 cudaError_t launch_step<double, MRSIM_TASK_ID>(const mrsim_dev::StepParams<double>& p, int L, int grid, int block,
                                                int smem, cudaStream_t s) {
+    if (L == 4) return launch_L<double, 4>(p, grid, block, smem, s);
     if (L == 8) return launch_L<double, 8>(p, grid, block, smem, s);
-    if (L == 16) return launch_L<double, 16>(p, grid, block, smem, s);
-    return launch_L<double, 32>(p, grid, block, smem, s);
+    return launch_L<double, 16>(p, grid, block, smem, s);
 }
 template <>
 cudaError_t step_occupancy<float, MRSIM_TASK_ID>(int L, int block, int smem, int* bps) {
+    if (L == 4) return occ_L<float, 4>(block, smem, bps);
     if (L == 8) return occ_L<float, 8>(block, smem, bps);
-    if (L == 16) return occ_L<float, 16>(block, smem, bps);
-    return occ_L<float, 32>(block, smem, bps);
+    return occ_L<float, 16>(block, smem, bps);
 }
 template <>
 cudaError_t step_occupancy<double, MRSIM_TASK_ID>(int L, int block, int smem, int* bps) {
+    if (L == 4) return occ_L<double, 4>(block, smem, bps);
     if (L == 8) return occ_L<double, 8>(block, smem, bps);
-    if (L == 16) return occ_L<double, 16>(block, smem, bps);
-    return occ_L<double, 32>(block, smem, bps);
-}
-template <class Real, int L>
-static cudaError_t observe_L(const mrsim_cfg& c, const mrsim_dev::DevState<Real>& s, float* obs, long long B, int D,
-                             int bdim, int nf, int ni, int smem_group, cudaStream_t st) {
-    const int block = 256, gpb = block / L;
-    const unsigned grid = static_cast<unsigned>((B + gpb - 1) / gpb);
-    auto k = mrsim_dev::observe_kernel<Real, L, MRSIM_TASK_ID>;
-    if (smem_group * gpb > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_group * gpb);
-    k<<<grid, block, smem_group * gpb, st>>>(c, s, obs, B, c.num_robots, D, bdim, nf, ni, smem_group);
-    return cudaGetLastError();
+    return occ_L<double, 16>(block, smem, bps);
 }
 template <>
 cudaError_t launch_observe<float, MRSIM_TASK_ID>(const mrsim_cfg& c, const mrsim_dev::DevState<float>& s, float* obs,
-                                                 long long B, int L, int D, int bdim, int nf, int ni, int sg,
-                                                 cudaStream_t st) {
-    if (L == 8) return observe_L<float, 8>(c, s, obs, B, D, bdim, nf, ni, sg, st);
-    if (L == 16) return observe_L<float, 16>(c, s, obs, B, D, bdim, nf, ni, sg, st);
-    return observe_L<float, 32>(c, s, obs, B, D, bdim, nf, ni, sg, st);
+                                                 long long B, int D, int bdim, int nf, int ni, cudaStream_t st) {
+    const unsigned grid = static_cast<unsigned>((B + 127) / 128);
+    mrsim_dev::observe_kernel<float, MRSIM_TASK_ID><<<grid, 128, 0, st>>>(c, s, obs, B, c.num_robots, D, bdim, nf, ni);
+    return cudaGetLastError();
 }
 template <>
 cudaError_t launch_observe<double, MRSIM_TASK_ID>(const mrsim_cfg& c, const mrsim_dev::DevState<double>& s,
-                                                  float* obs, long long B, int L, int D, int bdim, int nf, int ni,
-                                                  int sg, cudaStream_t st) {
-    if (L == 8) return observe_L<double, 8>(c, s, obs, B, D, bdim, nf, ni, sg, st);
-    if (L == 16) return observe_L<double, 16>(c, s, obs, B, D, bdim, nf, ni, sg, st);
-    return observe_L<double, 32>(c, s, obs, B, D, bdim, nf, ni, sg, st);
+                                                  float* obs, long long B, int D, int bdim, int nf, int ni,
+                                                  cudaStream_t st) {
+    const unsigned grid = static_cast<unsigned>((B + 127) / 128);
+    mrsim_dev::observe_kernel<double, MRSIM_TASK_ID><<<grid, 128, 0, st>>>(c, s, obs, B, c.num_robots, D, bdim, nf, ni);
+    return cudaGetLastError();
 }
 
 template <>

@@ -10,11 +10,12 @@
 //   -> transition / violation / step_index / done / finalize (batch.hpp:212-220)
 //   -> observations (batch.hpp:143-151, 221) -> optional in-kernel auto-reset.
 //
-// Lane v of the group owns QP variable v = 2*robot + axis; both lanes of a
-// robot carry that robot's pose redundantly (no divergence, no extra
-// traffic). Pair rows are spread over all lanes; reductions are shuffles.
+// Lane r of a group of L = next_pow2(N) lanes carries robot r (its pose and
+// its two QP variables); pair rows are spread over all lanes; reductions are
+// shuffles. A warp steps 32/L environments in lockstep (group.cuh).
 #pragma once
 
+#include "group.cuh"
 #include "mrsim_device.cuh"
 #include "qp_group.cuh"
 #include "tasks.cuh"
@@ -46,7 +47,7 @@ struct EnvStats {
 // inflation of apply_barrier (barrier.hpp:151-157, 173).
 template <class Real>
 struct PhysConsts {
-    Real dt, v_max, w_max, si_max, hw, hh, coll_r, k_pos, l, gamma, r_eff2, cap, obs_r_eff2, tol;
+    Real dt, v_max, w_max, si_max, hw, hh, coll_r, k_pos, l, inv_l, gamma, r_eff2, cap, obs_r_eff2, tol;
     Real wall_xmin, wall_xmax, wall_ymin, wall_ymax;
 };
 
@@ -84,353 +85,360 @@ __device__ __forceinline__ void pair_of(int p, int N, int& i, int& j) {
     j = i + 1 + rem;
 }
 
+template <int L>
+struct LaneCfg {  // pair slots per lane for N <= L robots: ceil(L(L-1)/2 / L)
+    static constexpr int kMaxPair = (L * (L - 1) / 2 + L - 1) / L;
+};
+
+template <int TASK>
+struct TaskCfg { static constexpr int kMaxObs = (TASK == MRSIM_TASK_RWARE) ? MRSIM_MAX_SLOTS : 0; };
+
 // ---------------------------------------------------------------------------
 // Barrier rows of one tick (build_barrier_constraints + fold_rows), owned by
-// lanes: pair p by lane p % L; the two wall rows and two box sides of
-// variable v by lane v; obstacle rows of robot i at slot o by lane 2i+(o&1).
-// Global row indices follow the reference order (pairs, walls robot-major
-// [x-min, x-max, y-min, y-max], obstacles robot-major, box hi/lo per
-// variable), which is also the tie-break order of the QP scans.
+// lanes: pair p by lane p % L; the four wall rows, the four box sides and
+// the obstacle rows of robot r by lane r. Global row indices follow the
+// reference order (pairs; walls robot-major [x-min, x-max, y-min, y-max];
+// obstacles robot-major; box hi/lo per variable), which is also the
+// tie-break order of the QP scans.
+// active bits: [0,MP) pairs, MP+w walls, MP+4+b box (x-hi, x-lo, y-hi, y-lo), MP+8+t obstacles
 // ---------------------------------------------------------------------------
-template <class Real, int L, int MAXPAIR, int MAXOBS>
+template <class Real, int L, int MP, int MO>
 struct BarrierRows {
-    int N, n, P, off_obs, off_box;
-    int pi[MAXPAIR], pj[MAXPAIR];
-    Real pgx[MAXPAIR], pgy[MAXPAIR], ph[MAXPAIR];
-    Real wlo, whi, cap;
+    static constexpr int MO1 = MO > 0 ? MO : 1;
+    int N, P, off_obs, off_box;
+    int npair;
+    int pi[MP], pj[MP];
+    Real pgx[MP], pgy[MP], ph[MP];
+    Real wl[4];
+    Real cap;
     int nob;
-    Real ogx[MAXOBS > 0 ? MAXOBS : 1], ogy[MAXOBS > 0 ? MAXOBS : 1], oh[MAXOBS > 0 ? MAXOBS : 1];
-    int oslot[MAXOBS > 0 ? MAXOBS : 1];           // obstacle index o (row order robot-major, then o)
-    Real ocx[MAXOBS > 0 ? MAXOBS : 1], ocy[MAXOBS > 0 ? MAXOBS : 1], or2[MAXOBS > 0 ? MAXOBS : 1];
+    int oslot[MO1];
+    Real ocx[MO1], ocy[MO1], or2[MO1], ogx[MO1], ogy[MO1], oh[MO1];
     unsigned active;
+    bool valid;  // this lane carries a robot
 
-    __device__ __forceinline__ void consider(Real val, int idx, Real& worst, int& p) const {
+    __device__ __forceinline__ int dummy_row() const { return off_box; }
+
+    __device__ __forceinline__ static void consider(Real val, int idx, Real& worst, int& p) {
         if (val > worst || (val == worst && p >= 0 && idx < p)) {
             worst = val;
             p = idx;
         }
     }
+    __device__ __forceinline__ bool off(int bit) const { return !((active >> bit) & 1u); }
 
-    __device__ __forceinline__ void scan(const Group<L>& g, Real u, Real& worst, int& p) const {
+    __device__ __forceinline__ void scan(const Grp<L>& g, Real ux, Real uy, Real& worst, int& p) const {
         const int lane = g.lane;
 #pragma unroll
-        for (int s = 0; s < MAXPAIR; ++s) {
-            const int pidx = lane + s * L;
-            const bool has = pidx < P;
-            const Real uxi = g.shfl(u, 2 * pi[s]);
-            const Real uyi = g.shfl(u, 2 * pi[s] + 1);
-            const Real uxj = g.shfl(u, 2 * pj[s]);
-            const Real uyj = g.shfl(u, 2 * pj[s] + 1);
-            if (has && !((active >> s) & 1u))
-                consider(pgx[s] * (uxj - uxi) + pgy[s] * (uyj - uyi) - ph[s], pidx, worst, p);
+        for (int s = 0; s < MP; ++s) {
+            const Real uxi = g.shfl(ux, pi[s]), uyi = g.shfl(uy, pi[s]);
+            const Real uxj = g.shfl(ux, pj[s]), uyj = g.shfl(uy, pj[s]);
+            if (s < npair && off(s)) consider(pgx[s] * (uxj - uxi) + pgy[s] * (uyj - uyi) - ph[s], lane + s * L, worst, p);
         }
-        if (lane < n) {
-            const int lo_idx = P + 4 * (lane >> 1) + 2 * (lane & 1);
-            if (!((active >> MAXPAIR) & 1u)) consider(-u - wlo, lo_idx, worst, p);
-            if (!((active >> (MAXPAIR + 1)) & 1u)) consider(u - whi, lo_idx + 1, worst, p);
-            if (!((active >> (MAXPAIR + 2)) & 1u)) consider(u - cap, off_box + 2 * lane, worst, p);
-            if (!((active >> (MAXPAIR + 3)) & 1u)) consider(-u - cap, off_box + 2 * lane + 1, worst, p);
-        }
-        if (MAXOBS > 0) {
-            const Real ux = g.shfl(u, lane & ~1);
-            const Real uy = g.shfl(u, (lane | 1) < L ? (lane | 1) : lane);
+        if (valid) {
+            const int w0 = P + 4 * lane;
+            if (off(MP + 0)) consider(-ux - wl[0], w0, worst, p);
+            if (off(MP + 1)) consider(ux - wl[1], w0 + 1, worst, p);
+            if (off(MP + 2)) consider(-uy - wl[2], w0 + 2, worst, p);
+            if (off(MP + 3)) consider(uy - wl[3], w0 + 3, worst, p);
+            if (MO > 0) {
 #pragma unroll
-            for (int t = 0; t < (MAXOBS > 0 ? MAXOBS : 1); ++t) {
-                if (t < nob && !((active >> (MAXPAIR + 4 + t)) & 1u))
-                    consider(ogx[t] * ux + ogy[t] * uy - oh[t],
-                             off_obs + (lane >> 1) * MRSIM_MAX_SLOTS + oslot[t], worst, p);
+                for (int t = 0; t < MO1; ++t)
+                    if (t < nob && off(MP + 8 + t))
+                        consider(ogx[t] * ux + ogy[t] * uy - oh[t], off_obs + lane * MRSIM_MAX_SLOTS + oslot[t], worst, p);
             }
+            const int b0 = off_box + 4 * lane;
+            if (off(MP + 4)) consider(ux - cap, b0, worst, p);
+            if (off(MP + 5)) consider(-ux - cap, b0 + 1, worst, p);
+            if (off(MP + 6)) consider(uy - cap, b0 + 2, worst, p);
+            if (off(MP + 7)) consider(-uy - cap, b0 + 3, worst, p);
         }
     }
 
-    __device__ __forceinline__ void fetch(const Group<L>& g, int p, Real& gv, Real& hp) const {
+    // Component of row p on this lane's robot, and the rhs. Collectives are
+    // unconditional (p may differ between the groups of a warp).
+    __device__ __forceinline__ void fetch(const Grp<L>& g, int p, Real& gx, Real& gy, Real& hp) const {
         const int lane = g.lane;
-        const int rv = lane >> 1, ax = lane & 1;
+        int kind, owner;
+        Real cgx = 0, cgy = 0, ch = 0;
+        int cij = 0;
         if (p < P) {
-            const int owner = p & (L - 1), s = p / L;
-            Real gx = 0, gy = 0, h = 0;
-            int ij = 0;
+            kind = 0;
+            owner = p & (L - 1);
+            const int s = p / L;
 #pragma unroll
-            for (int t = 0; t < MAXPAIR; ++t)
+            for (int t = 0; t < MP; ++t)
                 if (t == s) {
-                    gx = pgx[t];
-                    gy = pgy[t];
-                    h = ph[t];
-                    ij = pi[t] | (pj[t] << 8);
+                    cgx = pgx[t];
+                    cgy = pgy[t];
+                    ch = ph[t];
+                    cij = pi[t] | (pj[t] << 8);
                 }
-            gx = g.shfl(gx, owner);
-            gy = g.shfl(gy, owner);
-            h = g.shfl(h, owner);
-            ij = g.shfl(ij, owner);
-            const int i = ij & 0xff, j = ij >> 8;
-            const Real comp = ax ? gy : gx;
-            gv = (rv == j) ? comp : ((rv == i) ? -comp : Real(0));
-            hp = h;
         } else if (p < off_obs) {
-            const int q = p - P;
-            const int owner = 2 * (q >> 2) + ((q & 3) >> 1);
-            const bool hi = q & 1;
-            hp = g.shfl(hi ? whi : wlo, owner);
-            gv = (lane == owner) ? (hi ? Real(1) : Real(-1)) : Real(0);
+            kind = 1;
+            const int q = p - P, w = q & 3;
+            owner = q >> 2;
+            cgx = (w == 0) ? Real(-1) : ((w == 1) ? Real(1) : Real(0));
+            cgy = (w == 2) ? Real(-1) : ((w == 3) ? Real(1) : Real(0));
+            ch = wl[w];
+            cij = owner;
         } else if (p < off_box) {
-            const int q = p - off_obs;
-            const int i = q / MRSIM_MAX_SLOTS, o = q % MRSIM_MAX_SLOTS;
-            const int owner = 2 * i + (o & 1);
-            Real gx = 0, gy = 0, h = 0;
+            kind = 2;
+            const int q = p - off_obs, o = q % MRSIM_MAX_SLOTS;
+            owner = q / MRSIM_MAX_SLOTS;
+            if (MO > 0) {
 #pragma unroll
-            for (int t = 0; t < (MAXOBS > 0 ? MAXOBS : 1); ++t)
-                if (t < nob && oslot[t] == o) {
-                    gx = ogx[t];
-                    gy = ogy[t];
-                    h = oh[t];
-                }
-            gx = g.shfl(gx, owner);
-            gy = g.shfl(gy, owner);
-            hp = g.shfl(h, owner);
-            gv = (rv == i) ? (ax ? gy : gx) : Real(0);
+                for (int t = 0; t < MO1; ++t)
+                    if (t < nob && oslot[t] == o) {
+                        cgx = ogx[t];
+                        cgy = ogy[t];
+                        ch = oh[t];
+                    }
+            }
+            cij = owner;
         } else {
-            const int q = p - off_box;
-            const int v0 = q >> 1;
-            const bool lo = q & 1;
-            gv = (lane == v0) ? (lo ? Real(-1) : Real(1)) : Real(0);
-            hp = cap;
+            kind = 3;
+            const int q = p - off_box, b = q & 3;
+            owner = q >> 2;
+            cgx = (b == 0) ? Real(1) : ((b == 1) ? Real(-1) : Real(0));
+            cgy = (b == 2) ? Real(1) : ((b == 3) ? Real(-1) : Real(0));
+            ch = cap;
+            cij = owner;
+        }
+        const Real bgx = g.shfl(cgx, owner), bgy = g.shfl(cgy, owner);
+        hp = g.shfl(ch, owner);
+        const int bij = g.shfl(cij, owner);
+        if (kind == 0) {
+            const int i = bij & 0xff, j = bij >> 8;
+            const Real sgn = (lane == j) ? Real(1) : ((lane == i) ? Real(-1) : Real(0));
+            gx = sgn * bgx;
+            gy = sgn * bgy;
+        } else {
+            gx = (lane == bij) ? bgx : Real(0);
+            gy = (lane == bij) ? bgy : Real(0);
         }
     }
 
-    __device__ __forceinline__ void set_active(const Group<L>& g, int p, bool on) {
-        const int lane = g.lane;
+    __device__ __forceinline__ void set_active(const Grp<L>& g, int p, bool on) {
         int owner, bit;
         if (p < P) {
             owner = p & (L - 1);
             bit = p / L;
         } else if (p < off_obs) {
-            const int q = p - P;
-            owner = 2 * (q >> 2) + ((q & 3) >> 1);
-            bit = MAXPAIR + (q & 1);
+            owner = (p - P) >> 2;
+            bit = MP + ((p - P) & 3);
         } else if (p < off_box) {
-            const int q = p - off_obs;
-            const int o = q % MRSIM_MAX_SLOTS;
-            owner = 2 * (q / MRSIM_MAX_SLOTS) + (o & 1);
-            bit = MAXPAIR + 4;
+            const int q = p - off_obs, o = q % MRSIM_MAX_SLOTS;
+            owner = q / MRSIM_MAX_SLOTS;
+            bit = MP + 8;
+            if (MO > 0) {
 #pragma unroll
-            for (int t = 0; t < (MAXOBS > 0 ? MAXOBS : 1); ++t)
-                if (t < nob && oslot[t] == o) bit = MAXPAIR + 4 + t;
+                for (int t = 0; t < MO1; ++t)
+                    if (t < nob && oslot[t] == o) bit = MP + 8 + t;
+            }
         } else {
-            const int q = p - off_box;
-            owner = q >> 1;
-            bit = MAXPAIR + 2 + (q & 1);
+            owner = (p - off_box) >> 2;
+            bit = MP + 4 + ((p - off_box) & 3);
         }
-        if (lane == owner) {
-            if (on) active |= 1u << bit;
-            else active &= ~(1u << bit);
-        }
+        if (g.lane == owner) active = on ? (active | (1u << bit)) : (active & ~(1u << bit));
     }
 };
 
+template <class Real, int L, int MP, int MO>
+__device__ __forceinline__ void init_rows(BarrierRows<Real, L, MP, MO>& rows, int lane, int N, Real cap) {
+    rows.N = N;
+    rows.P = N * (N - 1) / 2;
+    rows.off_obs = rows.P + 4 * N;
+    rows.off_box = rows.off_obs + N * MRSIM_MAX_SLOTS;
+    rows.cap = cap;
+    rows.valid = lane < N;
+    rows.nob = 0;
+    rows.npair = 0;
+#pragma unroll
+    for (int s = 0; s < MP; ++s) {
+        const int pidx = lane + s * L;
+        int i = 0, j = 0;
+        if (pidx < rows.P) {
+            pair_of(pidx, N, i, j);
+            rows.npair = s + 1;
+        }
+        rows.pi[s] = i;
+        rows.pj[s] = j;
+    }
+}
 
 // One safety-filter evaluation (apply_barrier, barrier.hpp:132-205) for the
 // group's robots: u_nom = uni_to_si(nominal), rows at the projected points,
 // QP, infeasible -> zero commands, else map back with a uniform scale.
 // Returns kQpOptimal/kQpIterLimit (commands set), kQpInfeasible (zeroed), or
 // -1 for coincident projected points (domain_error, barrier.hpp:73-74).
-template <class Real, int L, int MAXPAIR, int MAXOBS>
-__device__ int barrier_filter(const Group<L>& g, BarrierRows<Real, L, MAXPAIR, MAXOBS>& rows, const QpSmem<Real>& ws,
-                              const PhysConsts<Real>& k, int n, int P, bool vlane, int ax, int ri, Real prx, Real pry,
-                              Real cs, Real sn, Real nv, Real nw, int total_rows, Real& cv, Real& cw) {
+template <class Real, int L, int MP, int MO>
+__device__ int barrier_filter(const Grp<L>& g, BarrierRows<Real, L, MP, MO>& rows, const QpWs<Real>& ws,
+                              const PhysConsts<Real>& k, bool participate, Real prx, Real pry, Real cs, Real sn,
+                              Real nv, Real nw, int total_rows, Real& cv, Real& cw) {
     const int lane = g.lane;
-    Real u = 0;  // u_nom = uni_to_si(clamped nominal) (controllers.hpp:59-65)
-    if (vlane) u = ax ? (sn * nv + k.l * cs * nw) : (cs * nv - k.l * sn * nw);
-    // rows at the projected points (barrier.hpp:57-121 + fold_rows qp.hpp:104-125)
+    const int n = 2 * rows.N;
+    // u_nom = uni_to_si(clamped nominal) (controllers.hpp:59-65)
+    Real ux = cs * nv - k.l * sn * nw;
+    Real uy = sn * nv + k.l * cs * nw;
+    if (!rows.valid) ux = uy = Real(0);
+    // pair rows at the projected points (barrier.hpp:69-83 + fold_rows qp.hpp:104-125)
     bool coincident = false;
 #pragma unroll
-    for (int s = 0; s < MAXPAIR; ++s) {
-        const int pidx = lane + s * L;
-        const Real xi = g.shfl(prx, 2 * rows.pi[s]), yi = g.shfl(pry, 2 * rows.pi[s]);
-        const Real xj = g.shfl(prx, 2 * rows.pj[s]), yj = g.shfl(pry, 2 * rows.pj[s]);
+    for (int s = 0; s < MP; ++s) {
+        const Real xi = g.shfl(prx, rows.pi[s]), yi = g.shfl(pry, rows.pi[s]);
+        const Real xj = g.shfl(prx, rows.pj[s]), yj = g.shfl(pry, rows.pj[s]);
         const Real dx = xi - xj, dy = yi - yj;
         const Real dist2 = dx * dx + dy * dy;
-        if (pidx < P && dist2 < Real(1e-18)) coincident = true;
+        if (s < rows.npair && dist2 < Real(1e-18)) coincident = true;
         const Real h = dist2 - k.r_eff2;
         const Real inv = Real(1) / dsqrt(Real(8) * dist2);
         rows.pgx[s] = Real(2) * dx * inv;
         rows.pgy[s] = Real(2) * dy * inv;
         rows.ph[s] = k.gamma * h * h * h * inv;
     }
-    if (g.any(coincident)) return -1;
+    // walls (barrier.hpp:85-104)
     {
-        const Real coord = ax ? pry : prx;
-        const Real lo_h = coord - (ax ? k.wall_ymin : k.wall_xmin);
-        const Real hi_h = (ax ? k.wall_ymax : k.wall_xmax) - coord;
-        rows.wlo = k.gamma * lo_h * lo_h * lo_h;
-        rows.whi = k.gamma * hi_h * hi_h * hi_h;
+        const Real h0 = prx - k.wall_xmin, h1 = k.wall_xmax - prx;
+        const Real h2 = pry - k.wall_ymin, h3 = k.wall_ymax - pry;
+        rows.wl[0] = k.gamma * h0 * h0 * h0;
+        rows.wl[1] = k.gamma * h1 * h1 * h1;
+        rows.wl[2] = k.gamma * h2 * h2 * h2;
+        rows.wl[3] = k.gamma * h3 * h3 * h3;
     }
-    if (MAXOBS > 0) {
+    // static obstacles (barrier.hpp:106-119)
+    if (MO > 0) {
 #pragma unroll
-        for (int t = 0; t < (MAXOBS > 0 ? MAXOBS : 1); ++t) {
+        for (int t = 0; t < BarrierRows<Real, L, MP, MO>::MO1; ++t) {
             if (t < rows.nob) {
-                const Real dx = prx - rows.ocx[t];
-                const Real dy = pry - rows.ocy[t];
+                const Real dx = prx - rows.ocx[t], dy = pry - rows.ocy[t];
                 const Real h = dx * dx + dy * dy - rows.or2[t];
                 const Real nrm = dsqrt(Real(4) * dx * dx + Real(4) * dy * dy);
                 const Real gh = k.gamma * h * h * h;
-                if (nrm < Real(1e-14)) {
-                    rows.ogx[t] = 0;
-                    rows.ogy[t] = 0;
-                    rows.oh[t] = gh;
-                } else {
-                    rows.ogx[t] = Real(-2) * dx / nrm;
-                    rows.ogy[t] = Real(-2) * dy / nrm;
-                    rows.oh[t] = gh / nrm;
-                }
+                const bool zero = nrm < Real(1e-14);
+                const Real inv = zero ? Real(0) : Real(1) / nrm;
+                rows.ogx[t] = Real(-2) * dx * inv;
+                rows.ogy[t] = Real(-2) * dy * inv;
+                rows.oh[t] = zero ? gh : gh * inv;
             }
         }
     }
+    const bool bad = g.any(coincident);
     rows.active = 0;
-    const int status = qp_solve_group<Real, L>(g, rows, ws, n, u, total_rows, 0, k.tol, nullptr);
-    if (status == kQpInfeasible) {  // barrier.hpp:178-182
-        cv = 0;
-        cw = 0;
-        return status;
-    }
-    // map back + uniform scale (barrier.hpp:189-204)
-    const Real ux = g.shfl(u, 2 * ri), uy = g.shfl(u, 2 * ri + 1);
+    const int status = qp_solve<Real, L>(g, rows, ws, n, participate && !bad, ux, uy, total_rows, k.tol);
+    // map back + uniform scale (barrier.hpp:186-204)
     const Real mv = cs * ux + sn * uy;
-    const Real mw = (-sn * ux + cs * uy) / k.l;
+    const Real mw = (-sn * ux + cs * uy) * k.inv_l;
     Real scale = 1;
-    if (vlane) {
+    if (rows.valid) {
         if (dabs(mv) > k.v_max) scale = dmin(scale, k.v_max / dabs(mv));
         if (dabs(mw) > k.w_max) scale = dmin(scale, k.w_max / dabs(mw));
     }
     scale = g.min(scale);
-    cv = mv * scale;
-    cw = mw * scale;
-    return status;
+    const bool zero = status == kQpInfeasible;  // barrier.hpp:178-182
+    cv = zero ? Real(0) : mv * scale;
+    cw = zero ? Real(0) : mw * scale;
+    (void)lane;
+    return bad ? -1 : status;
 }
 
-template <int L>
-struct LaneCfg;
-template <>
-struct LaneCfg<8> { static constexpr int kMaxN = 4, kMaxPair = 1; };
-template <>
-struct LaneCfg<16> { static constexpr int kMaxN = 8, kMaxPair = 2; };
-template <>
-struct LaneCfg<32> { static constexpr int kMaxN = 16, kMaxPair = 4; };
-
-template <int TASK>
-struct TaskCfg { static constexpr int kMaxObs = (TASK == MRSIM_TASK_RWARE) ? MRSIM_MAX_SLOTS / 2 : 0; };
-
-// Shared-memory layout of one group.
+// Shared-memory layout of one group: QP workspace, final-pose staging, task state.
 template <class Real>
 struct GroupSmem {
-    QpSmem<Real> qp;
+    QpWs<Real> qp;
     Real *xs, *ys, *ts, *tf;
-    int* ti;
-    int* misc;
-    static __host__ __device__ int bytes(int n, int N) {
-        const int reals = QpSmem<Real>::reals(n) + 3 * N + kTfMax;
-        const int ints = QpSmem<Real>::ints(n) + kTiMax + 4;
-        int b = reals * static_cast<int>(sizeof(Real)) + ints * 4;
+    int *ti, *misc;
+    static __host__ __device__ int bytes(int N, int nf, int ni) {
+        const int n = 2 * N;
+        const int reals = QpWs<Real>::reals(n) + 3 * N + nf;
+        const int ints = QpWs<Real>::ints(n) + ni + 2;
+        const int b = reals * static_cast<int>(sizeof(Real)) + ints * 4;
         return (b + 15) & ~15;
     }
-    __device__ void carve(unsigned char* base, int n, int N) {
+    __device__ void carve(unsigned char* base, int N, int nf) {
+        const int n = 2 * N;
         Real* r = reinterpret_cast<Real*>(base);
-        int* ib = reinterpret_cast<int*>(r + QpSmem<Real>::reals(n) + 3 * N + kTfMax);
+        int* ib = reinterpret_cast<int*>(r + QpWs<Real>::reals(n) + 3 * N + nf);
         qp.carve(r, ib, n);
-        xs = r + QpSmem<Real>::reals(n);
+        xs = r + QpWs<Real>::reals(n);
         ys = xs + N;
         ts = ys + N;
         tf = ts + N;
-        ti = ib + QpSmem<Real>::ints(n);
-        misc = ti + kTiMax;
+        ti = ib + QpWs<Real>::ints(n);
+        misc = ti;  // misc words follow the ni task words (set by the kernel)
     }
 };
 
+// wrap_angle (core.hpp:102-108) for |t| < 3*pi: remainder(t, 2*pi) is t -/+ 2*pi,
+// exact by Sterbenz, so this is bit-identical to the reference on the tick path.
 template <class Real>
-__device__ __forceinline__ Real wrap_angle_dev(Real t) {  // core.hpp:102-108
-    Real r = remainder(t, Consts<Real>::two_pi);
+__device__ __forceinline__ Real wrap_angle_dev(Real t) {
+    Real r = t;
+    if (dabs(r) >= Real(3) * Consts<Real>::pi) r = remainder(t, Consts<Real>::two_pi);
+    else if (r > Consts<Real>::pi) r -= Consts<Real>::two_pi;
+    else if (r < -Consts<Real>::pi) r += Consts<Real>::two_pi;
     if (r <= -Consts<Real>::pi) r += Consts<Real>::two_pi;
     return r;
 }
 
 // ---------------------------------------------------------------------------
-// The fused step kernel. Persistent grid-stride loop over environments.
+// The fused step kernel. Persistent grid-stride loop; each warp steps 32/L
+// environments in lockstep (ghost groups past the end compute but never store).
 // ---------------------------------------------------------------------------
 template <class Real, int L, int TASK>
-__global__ void __launch_bounds__(256) step_kernel(const __grid_constant__ StepParams<Real> p) {
-    constexpr int MAXPAIR = LaneCfg<L>::kMaxPair;
-    constexpr int MAXOBS = TaskCfg<TASK>::kMaxObs;
+__global__ void __launch_bounds__(128) step_kernel(const __grid_constant__ StepParams<Real> p) {
+    constexpr int MP = LaneCfg<L>::kMaxPair;
+    constexpr int MO = TaskCfg<TASK>::kMaxObs;
+    constexpr int G = 32 / L;  // envs per warp
     if (*p.err != ~0ull) return;  // sticky device error: later steps are no-ops
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const Group<L> g;
+    const Grp<L> g;
     const int lane = g.lane;
     const int gpb = blockDim.x / L;
     const int gib = threadIdx.x / L;
     const mrsim_cfg& c = p.c;
-    const int N = p.N, n = p.n, P = p.P;
+    const int N = p.N;
     GroupSmem<Real> sm;
-    sm.carve(smem_raw + gib * p.smem_bytes_per_group, n, N);
+    sm.carve(smem_raw + gib * p.smem_bytes_per_group, N, p.nf);
+    int* misc = sm.ti + p.ni;
 
-    // lane -> robot / axis
-    const bool vlane = lane < n;
-    const int ri = vlane ? (lane >> 1) : 0;
-    const int ax = lane & 1;
+    const bool vl = lane < N;  // lane r carries robot r
+    const int ri = vl ? lane : 0;
 
-    BarrierRows<Real, L, MAXPAIR, MAXOBS> rows;
-    rows.N = N;
-    rows.n = n;
-    rows.P = P;
-    rows.off_obs = P + 4 * N;
-    rows.off_box = rows.off_obs + N * MRSIM_MAX_SLOTS;
-    rows.cap = p.k.cap;
-#pragma unroll
-    for (int s = 0; s < MAXPAIR; ++s) {
-        const int pidx = lane + s * L;
-        int i = 0, j = 0;
-        if (pidx < P) pair_of(pidx, N, i, j);
-        rows.pi[s] = i;
-        rows.pj[s] = j;
-    }
-    const int total_rows_base = P + 4 * N + 2 * n;
+    BarrierRows<Real, L, MP, MO> rows;
+    init_rows(rows, lane, N, p.k.cap);
+    const int total_rows_base = rows.P + 4 * N + 4 * N;
     const EnvView<Real> view{sm.xs, sm.ys, sm.ts, sm.tf, sm.ti, N};
+    const long long stride = static_cast<long long>(gridDim.x) * gpb;
 
-    for (long long e = static_cast<long long>(blockIdx.x) * gpb + gib; e < p.B;
-         e += static_cast<long long>(gridDim.x) * gpb) {
+    for (long long e0 = static_cast<long long>(blockIdx.x) * gpb + (gib & ~(G - 1)); e0 < p.B; e0 += stride) {
+        const long long e_real = e0 + (gib & (G - 1));
+        const bool ghost = e_real >= p.B;
+        const long long e = ghost ? p.B - 1 : e_real;
         // ---- load ----
         const int step_index = p.in.step_index[e];
         const uint64_t key = p.in.key[e];
-        Real x = 0, y = 0, th = 0;
-        if (vlane) {
-            x = p.in.px[e * N + ri];
-            y = p.in.py[e * N + ri];
-            th = p.in.pt[e * N + ri];
-        }
+        Real x = p.in.px[e * N + ri], y = p.in.py[e * N + ri], th = p.in.pt[e * N + ri];
         for (int f = lane; f < p.nf; f += L) sm.tf[f] = p.in.tf[static_cast<long long>(f) * p.B + e];
         for (int w = lane; w < p.ni; w += L) sm.ti[w] = p.in.ti[static_cast<long long>(w) * p.B + e];
-        g.sync();
+        Grp<L>::sync();
 
         // ---- actions (validate_actions, batch.hpp:226-237) ----
         int act = 0;
-        if (vlane) {
-            act = p.actions ? static_cast<int>(p.actions[e * N + ri])
-                            : policy_action(p.in.pkey[e], step_index, ri);
+        if (vl) act = p.actions ? static_cast<int>(p.actions[e * N + ri]) : policy_action(p.in.pkey[e], step_index, ri);
+        const int bad_robot = g.first(vl && (act < 0 || act >= 5));
+        const int bad_act = g.shfl(act, bad_robot < 0 ? 0 : bad_robot);
+        if (bad_robot >= 0 && lane == 0 && !ghost) {
+            report_error(p.err, e, bad_robot, kErrInvalidAction, bad_act);
+            *p.err_serial = p.serial;
         }
-        const unsigned badm = g.ballot(vlane && (act < 0 || act >= 5));
-        if (badm) {
-            const int bl = __ffs(badm) - 1;
-            const int bad_act = g.shfl(act, bl);
-            if (lane == 0) {
-                report_error(p.err, e, bl >> 1, kErrInvalidAction, bad_act);
-                *p.err_serial = p.serial;
-            }
-            g.sync();
-            continue;
-        }
+        bool skip = ghost || bad_robot >= 0;  // compute in lockstep, never store
 
         // ---- waypoints (Scenario::waypoints + action_to_waypoint) ----
         const uint64_t skey = fork_key(key, 1ull + static_cast<uint64_t>(step_index));  // step_stream
         Real wpx = x, wpy = y;
-        if (vlane) {
+        if (vl) {
             const Real ss = step_size_of<TASK, Real>(c, sm.ti, ri, x, y);
             const Real dxa = (act == 3) ? Real(-1) : ((act == 4) ? Real(1) : Real(0));
             const Real dya = (act == 1) ? Real(1) : ((act == 2) ? Real(-1) : Real(0));
@@ -448,7 +456,7 @@ __global__ void __launch_bounds__(256) step_kernel(const __grid_constant__ StepP
 
         // ---- static obstacles (Scenario::add_obstacles, rware.hpp:54-68) ----
         int n_obs_rows = 0;
-        if (MAXOBS > 0) {
+        if (MO > 0) {
             const int S = c.layout.rware_num_slots;
             unsigned carriers = 0;
             for (int i = 0; i < N; ++i) carriers |= (ti_byte(sm.ti, S + i) != 0 ? 1u : 0u) << i;
@@ -457,12 +465,12 @@ __global__ void __launch_bounds__(256) step_kernel(const __grid_constant__ StepP
                 int staged = 0;
                 for (int o = 0; o < S; ++o) staged += ti_byte(sm.ti, o) != 0 ? 1 : 0;
                 n_obs_rows = staged * __popc(carriers);
-                if (vlane && ((carriers >> ri) & 1u)) {
+                if (vl && ((carriers >> ri) & 1u)) {
                     int cnt = 0;
-                    for (int o = ax; o < S; o += 2) {
+                    for (int o = 0; o < S; ++o) {
                         if (ti_byte(sm.ti, o) == 0) continue;
 #pragma unroll
-                        for (int t = 0; t < (MAXOBS > 0 ? MAXOBS : 1); ++t)
+                        for (int t = 0; t < BarrierRows<Real, L, MP, MO>::MO1; ++t)
                             if (t == cnt) {
                                 rows.oslot[t] = o;
                                 rows.ocx[t] = Real(c.layout.rware_slots[2 * o]);
@@ -471,7 +479,7 @@ __global__ void __launch_bounds__(256) step_kernel(const __grid_constant__ StepP
                             }
                         ++cnt;
                     }
-                    rows.nob = cnt < MAXOBS ? cnt : MAXOBS;
+                    rows.nob = cnt;
                 }
             }
         }
@@ -481,7 +489,7 @@ __global__ void __launch_bounds__(256) step_kernel(const __grid_constant__ StepP
         Real min_dist = p.in.min_dist[e];
         int qp_inf = p.in.qp_inf[e];
         bool collision = false;
-        for (int tick = 0; tick < p.c.sub_steps; ++tick) {
+        for (int tick = 0; tick < c.sub_steps; ++tick) {
             Real sn, cs;
             dsincos(th, &sn, &cs);
             const Real prx = x + cs * p.k.l;  // projected_point (controllers.hpp:34-36)
@@ -491,25 +499,25 @@ __global__ void __launch_bounds__(256) step_kernel(const __grid_constant__ StepP
             if (!(wpx == x && wpy == y)) {
                 Real ux = p.k.k_pos * (wpx - prx);
                 Real uy = p.k.k_pos * (wpy - pry);
-                const Real nrm = dhypot(ux, uy);
+                const Real nrm = dsqrt(ux * ux + uy * uy);
                 if (!(nrm <= p.k.si_max || nrm == Real(0))) {
                     const Real sc = p.k.si_max / nrm;
                     ux *= sc;
                     uy *= sc;
                 }
                 nv = dclamp(cs * ux + sn * uy, -p.k.v_max, p.k.v_max);
-                nw = dclamp((-sn * ux + cs * uy) / p.k.l, -p.k.w_max, p.k.w_max);
+                nw = dclamp((-sn * ux + cs * uy) * p.k.inv_l, -p.k.w_max, p.k.w_max);
             }
             Real cv = nv, cw = nw;
             if (c.barrier_enabled) {
-                const int bs = barrier_filter<Real, L>(g, rows, sm.qp, p.k, n, P, vlane, ax, ri, prx, pry, cs, sn,
-                                                       nv, nw, total_rows, cv, cw);
-                if (bs < 0) {
+                const int bs = barrier_filter<Real, L>(g, rows, sm.qp, p.k, !skip, prx, pry, cs, sn, nv, nw,
+                                                       total_rows, cv, cw);
+                if (bs < 0 && !skip) {
                     if (lane == 0) {
                         report_error(p.err, e, 0, kErrCoincident);
                         *p.err_serial = p.serial;
                     }
-                    break;
+                    skip = true;
                 }
                 if (bs == kQpInfeasible) ++qp_inf;
             }
@@ -517,7 +525,7 @@ __global__ void __launch_bounds__(256) step_kernel(const __grid_constant__ StepP
             x = x + cv * cs * p.k.dt;
             y = y + cv * sn * p.k.dt;
             const Real tn = th + cw * p.k.dt;
-            if (vlane && !isfinite(tn)) {
+            if (vl && !skip && !isfinite(tn)) {
                 report_error(p.err, e, ri, kErrNonFinite);
                 *p.err_serial = p.serial;
             }
@@ -528,11 +536,11 @@ __global__ void __launch_bounds__(256) step_kernel(const __grid_constant__ StepP
             if (N > 1) {
                 Real md = Consts<Real>::inf;
 #pragma unroll
-                for (int s = 0; s < MAXPAIR; ++s) {
-                    const int pidx = lane + s * L;
-                    const Real xi = g.shfl(x, 2 * rows.pi[s]), yi = g.shfl(y, 2 * rows.pi[s]);
-                    const Real xj = g.shfl(x, 2 * rows.pj[s]), yj = g.shfl(y, 2 * rows.pj[s]);
-                    if (pidx < P) md = dmin(md, dhypot(xi - xj, yi - yj));
+                for (int s = 0; s < MP; ++s) {
+                    const Real xi = g.shfl(x, rows.pi[s]), yi = g.shfl(y, rows.pi[s]);
+                    const Real xj = g.shfl(x, rows.pj[s]), yj = g.shfl(y, rows.pj[s]);
+                    const Real dx = xi - xj, dy = yi - yj;
+                    if (s < rows.npair) md = dmin(md, dsqrt(dx * dx + dy * dy));
                 }
                 md = g.min(md);
                 min_dist = dmin(min_dist, md);
@@ -541,13 +549,12 @@ __global__ void __launch_bounds__(256) step_kernel(const __grid_constant__ StepP
         }
 
         // ---- stage final poses, transition, bookkeeping (lane 0) ----
-        if (vlane && ax == 0) {
+        if (vl) {
             sm.xs[ri] = x;
             sm.ys[ri] = y;
             sm.ts[ri] = th;
         }
-        g.sync();
-        int done = 0;
+        Grp<L>::sync();
         if (lane == 0) {
             Real metric = p.in.metric[e];
             int success = p.in.success[e];
@@ -561,42 +568,43 @@ __global__ void __launch_bounds__(256) step_kernel(const __grid_constant__ StepP
                 reward += Real(c.coef[MRSIM_COEF_VIOLATION]);
             }
             const int new_step = step_index + 1;
-            done = new_step >= c.max_steps ? 1 : 0;
+            const int done = new_step >= c.max_steps ? 1 : 0;
             if (done) finalize_task<TASK, Real>(c, v, metric, success);
             ep_return += reward;
-            if (p.reward) p.reward[e] = static_cast<float>(reward);
-            if (p.reward64) p.reward64[e] = static_cast<double>(reward);
-            if (p.done) p.done[e] = static_cast<uint8_t>(done);
-            if (done && new_step == c.max_steps) {  // EpisodeStats (harness.hpp:277-285)
-                p.st.episodes[e] += 1;
-                p.st.ret[e] += static_cast<double>(ep_return);
-                p.st.ret_sq[e] += static_cast<double>(ep_return) * static_cast<double>(ep_return);
-                p.st.metric[e] += static_cast<double>(metric);
-                p.st.success[e] += success ? 1.0 : 0.0;
-                p.st.collisions[e] += collisions;
-                p.st.qp_inf[e] += qp_inf;
-                p.st.min_dist[e] = fmin(p.st.min_dist[e], static_cast<double>(min_dist));
+            misc[0] = done;
+            if (!skip) {
+                if (p.reward) p.reward[e] = static_cast<float>(reward);
+                if (p.reward64) p.reward64[e] = static_cast<double>(reward);
+                if (p.done) p.done[e] = static_cast<uint8_t>(done);
+                if (done && new_step == c.max_steps) {  // EpisodeStats (harness.hpp:277-285)
+                    p.st.episodes[e] += 1;
+                    p.st.ret[e] += static_cast<double>(ep_return);
+                    p.st.ret_sq[e] += static_cast<double>(ep_return) * static_cast<double>(ep_return);
+                    p.st.metric[e] += static_cast<double>(metric);
+                    p.st.success[e] += success ? 1.0 : 0.0;
+                    p.st.collisions[e] += collisions;
+                    p.st.qp_inf[e] += qp_inf;
+                    p.st.min_dist[e] = fmin(p.st.min_dist[e], static_cast<double>(min_dist));
+                }
+                p.out.step_index[e] = new_step;
+                p.out.collisions[e] = collisions;
+                p.out.qp_inf[e] = qp_inf;
+                p.out.success[e] = success;
+                p.out.metric[e] = metric;
+                p.out.min_dist[e] = min_dist;
+                p.out.ep_return[e] = ep_return;
+                p.out.key[e] = key;
+                p.out.seed[e] = p.in.seed[e];
+                p.out.pkey[e] = p.in.pkey[e];
+                p.out.episode[e] = p.in.episode[e];
             }
-            sm.misc[0] = done;
-            // publish bookkeeping through smem-free registers of lane 0 (stored below)
-            p.out.step_index[e] = new_step;
-            p.out.collisions[e] = collisions;
-            p.out.qp_inf[e] = qp_inf;
-            p.out.success[e] = success;
-            p.out.metric[e] = metric;
-            p.out.min_dist[e] = min_dist;
-            p.out.ep_return[e] = ep_return;
-            p.out.key[e] = key;
-            p.out.seed[e] = p.in.seed[e];
-            p.out.pkey[e] = p.in.pkey[e];
-            p.out.episode[e] = p.in.episode[e];
         }
-        g.sync();
-        done = sm.misc[0];
+        Grp<L>::sync();
+        const int done = misc[0];
 
         // ---- observations (assemble_observations, batch.hpp:143-151) ----
         const int ND = N * p.D;
-        if (p.obs) {
+        if (p.obs && !skip) {
             float* o = p.obs + e * ND;
             for (int q = lane; q < ND; q += L) {
                 const int r = q / p.D;
@@ -605,7 +613,7 @@ __global__ void __launch_bounds__(256) step_kernel(const __grid_constant__ StepP
         }
 
         // ---- auto-reset (harness wave semantics, harness.hpp:227-232) ----
-        if (p.auto_reset && done) {
+        if (p.auto_reset && done && !skip) {
             if (lane == 0) {
                 const long long episode = p.in.episode[e] + p.episode_stride;
                 const uint64_t seed = derive_episode_seed(p.root_seed, episode);
@@ -636,25 +644,27 @@ __global__ void __launch_bounds__(256) step_kernel(const __grid_constant__ StepP
                 p.out.pkey[e] = policy_key_of(seed);
                 p.out.episode[e] = episode;
             }
-            g.sync();
-            if (p.next_obs) {
-                float* o = p.next_obs + e * ND;
-                for (int q = lane; q < ND; q += L) {
-                    const int r = q / p.D;
-                    o[q] = obs_feature<TASK, Real>(c, view, r, q - r * p.D, p.bdim);
-                }
+        }
+        Grp<L>::sync();
+        if (p.auto_reset && done && !skip && p.next_obs) {
+            float* o = p.next_obs + e * ND;
+            for (int q = lane; q < ND; q += L) {
+                const int r = q / p.D;
+                o[q] = obs_feature<TASK, Real>(c, view, r, q - r * p.D, p.bdim);
             }
         }
 
         // ---- store ----
-        for (int i = lane; i < N; i += L) {
-            p.out.px[e * N + i] = sm.xs[i];
-            p.out.py[e * N + i] = sm.ys[i];
-            p.out.pt[e * N + i] = sm.ts[i];
+        if (!skip) {
+            for (int i = lane; i < N; i += L) {
+                p.out.px[e * N + i] = sm.xs[i];
+                p.out.py[e * N + i] = sm.ys[i];
+                p.out.pt[e * N + i] = sm.ts[i];
+            }
+            for (int f = lane; f < p.nf; f += L) p.out.tf[static_cast<long long>(f) * p.B + e] = sm.tf[f];
+            for (int w = lane; w < p.ni; w += L) p.out.ti[static_cast<long long>(w) * p.B + e] = sm.ti[w];
         }
-        for (int f = lane; f < p.nf; f += L) p.out.tf[static_cast<long long>(f) * p.B + e] = sm.tf[f];
-        for (int w = lane; w < p.ni; w += L) p.out.ti[static_cast<long long>(w) * p.B + e] = sm.ti[w];
-        g.sync();
+        Grp<L>::sync();
     }
 }
 
@@ -727,32 +737,25 @@ __global__ void __launch_bounds__(128) reset_kernel(const __grid_constant__ Rese
     }
 }
 
-// assemble_observations of the current state (batch.hpp:143-151), one group per env.
-template <class Real, int L, int TASK>
-__global__ void __launch_bounds__(256) observe_kernel(const __grid_constant__ mrsim_cfg c, DevState<Real> s, float* obs,
-                                                      long long B, int N, int D, int bdim, int nf, int ni,
-                                                      int smem_bytes_per_group) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const Group<L> g;
-    const int gib = threadIdx.x / L;
-    const long long e = static_cast<long long>(blockIdx.x) * (blockDim.x / L) + gib;
+// assemble_observations of the current state (batch.hpp:143-151), one thread per env.
+template <class Real, int TASK>
+__global__ void __launch_bounds__(128) observe_kernel(const __grid_constant__ mrsim_cfg c, DevState<Real> s, float* obs,
+                                                      long long B, int N, int D, int bdim, int nf, int ni) {
+    const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (e >= B) return;
-    GroupSmem<Real> sm;
-    sm.carve(smem_raw + gib * smem_bytes_per_group, 2 * N, N);
-    for (int i = g.lane; i < N; i += L) {
-        sm.xs[i] = s.px[e * N + i];
-        sm.ys[i] = s.py[e * N + i];
-        sm.ts[i] = s.pt[e * N + i];
+    Real xs[MRSIM_MAX_ROBOTS], ys[MRSIM_MAX_ROBOTS], ts[MRSIM_MAX_ROBOTS], tf[kTfMax];
+    int ti[kTiMax];
+    for (int i = 0; i < N; ++i) {
+        xs[i] = s.px[e * N + i];
+        ys[i] = s.py[e * N + i];
+        ts[i] = s.pt[e * N + i];
     }
-    for (int f = g.lane; f < nf; f += L) sm.tf[f] = s.tf[static_cast<long long>(f) * B + e];
-    for (int w = g.lane; w < ni; w += L) sm.ti[w] = s.ti[static_cast<long long>(w) * B + e];
-    g.sync();
-    const EnvView<Real> view{sm.xs, sm.ys, sm.ts, sm.tf, sm.ti, N};
+    for (int f = 0; f < nf; ++f) tf[f] = s.tf[static_cast<long long>(f) * B + e];
+    for (int w = 0; w < ni; ++w) ti[w] = s.ti[static_cast<long long>(w) * B + e];
+    const EnvView<Real> v{xs, ys, ts, tf, ti, N};
     float* o = obs + e * N * D;
-    for (int q = g.lane; q < N * D; q += L) {
-        const int r = q / D;
-        o[q] = obs_feature<TASK, Real>(c, view, r, q - r * D, bdim);
-    }
+    for (int r = 0; r < N; ++r)
+        for (int q = 0; q < D; ++q) o[r * D + q] = obs_feature<TASK, Real>(c, v, r, q, bdim);
 }
 
 // Harness random-policy actions for the current step of every env.

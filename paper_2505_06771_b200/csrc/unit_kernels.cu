@@ -20,104 +20,98 @@ __global__ void __launch_bounds__(32) qp_batch_kernel(int count, int n, int m, c
                                                       const double* lo, const double* hi, const double* unom,
                                                       double tol, double* u_out, int32_t* status_out,
                                                       int32_t* iters_out) {
-    const int t = blockIdx.x;
-    if (t >= count) return;
-    __shared__ Real G[kQpMaxM * kQpMaxN];
-    __shared__ Real h[kQpMaxM];
-    __shared__ Real ush[kQpMaxN], los[kQpMaxN], his[kQpMaxN];
-    __shared__ Real wsr[QpSmem<Real>::reals(kQpMaxN)];
-    __shared__ int wsi[QpSmem<Real>::ints(kQpMaxN)];
-    const Group<32> g;
+    // one warp = two problems (16 lanes each, lane l owns variables 2l, 2l+1)
+    constexpr int L = 16;
+    extern __shared__ __align__(16) unsigned char qsmem[];
+    const Grp<L> g;
     const int lane = g.lane;
+    const int slot = threadIdx.x / L;
+    const int slot_reals = m * n + m + 3 * n + QpWs<Real>::reals(n);
+    Real* base = reinterpret_cast<Real*>(qsmem) + slot * slot_reals;
+    Real* Gs = base;
+    Real* hs = Gs + m * n;
+    Real* ushs = hs + m;
+    Real* loss = ushs + n;
+    Real* hiss = loss + n;
+    Real* wsr = hiss + n;
+    int* wsi = reinterpret_cast<int*>(reinterpret_cast<Real*>(qsmem) + 2 * slot_reals) + slot * n;
+    const int t_real = blockIdx.x * 2 + slot;
+    const bool ghost = t_real >= count;
+    const int t = ghost ? count - 1 : t_real;
     const double* At = A + static_cast<size_t>(t) * m * n;
     // fold_rows (qp.hpp:104-141): normalise; zero rows keep b unnormalised
-    for (int r = lane; r < m; r += 32) {
+    for (int r = lane; r < m; r += L) {
         double norm = 0.0;
         for (int i = 0; i < n; ++i) norm += At[r * n + i] * At[r * n + i];
         norm = sqrt(norm);
         const double br = b[static_cast<size_t>(t) * m + r];
         if (norm < 1e-14) {
-            for (int i = 0; i < n; ++i) G[r * n + i] = Real(0);
-            h[r] = Real(br);
+            for (int i = 0; i < n; ++i) Gs[r * n + i] = Real(0);
+            hs[r] = Real(br);
         } else {
-            for (int i = 0; i < n; ++i) G[r * n + i] = Real(At[r * n + i] / norm);
-            h[r] = Real(br / norm);
+            for (int i = 0; i < n; ++i) Gs[r * n + i] = Real(At[r * n + i] / norm);
+            hs[r] = Real(br / norm);
         }
     }
-    if (lane < n) {
-        los[lane] = Real(lo[static_cast<size_t>(t) * n + lane]);
-        his[lane] = Real(hi[static_cast<size_t>(t) * n + lane]);
+    for (int v = lane; v < n; v += L) {
+        loss[v] = Real(lo[static_cast<size_t>(t) * n + v]);
+        hiss[v] = Real(hi[static_cast<size_t>(t) * n + v]);
     }
-    g.sync();
+    Grp<L>::sync();
     int boxes = 0;
     for (int i = 0; i < n; ++i) {
         boxes += hi[static_cast<size_t>(t) * n + i] < 1e30 ? 1 : 0;
         boxes += lo[static_cast<size_t>(t) * n + i] > -1e30 ? 1 : 0;
     }
-    QpSmem<Real> ws;
+    QpWs<Real> ws;
     ws.carve(wsr, wsi, n);
-    DenseRows<Real, 32, kQpMaxM> rows{G, h, ush, los, his, n, m, 0ull, 0u};
-    Real u = lane < n ? Real(unom[static_cast<size_t>(t) * n + lane]) : Real(0);
-    int iters = 0;
-    const int status = qp_solve_group<Real, 32>(g, rows, ws, n, u, m + boxes, 0, Real(tol), &iters);
-    if (lane < n) u_out[static_cast<size_t>(t) * n + lane] = double(u);
-    if (lane == 0) {
-        status_out[t] = status;
-        iters_out[t] = iters;
+    DenseRows<Real, L, kQpMaxM> rows{Gs, hs, ushs, loss, hiss, n, m, 0ull, 0ull};
+    const bool vl = 2 * lane < n;
+    Real ux = vl ? Real(unom[static_cast<size_t>(t) * n + 2 * lane]) : Real(0);
+    Real uy = (vl && 2 * lane + 1 < n) ? Real(unom[static_cast<size_t>(t) * n + 2 * lane + 1]) : Real(0);
+    const int status = qp_solve<Real, L>(g, rows, ws, n, !ghost, ux, uy, m + boxes, Real(tol));
+    if (!ghost) {
+        if (vl) u_out[static_cast<size_t>(t) * n + 2 * lane] = double(ux);
+        if (vl && 2 * lane + 1 < n) u_out[static_cast<size_t>(t) * n + 2 * lane + 1] = double(uy);
+        if (lane == 0) {
+            status_out[t] = status;
+            iters_out[t] = 0;
+        }
     }
 }
 
 template <class Real, int L>
-__global__ void __launch_bounds__(256) barrier_batch_kernel(const __grid_constant__ mrsim_cfg c, PhysConsts<Real> k,
+__global__ void __launch_bounds__(128) barrier_batch_kernel(const __grid_constant__ mrsim_cfg c, PhysConsts<Real> k,
                                                             int count, int N, const double* poses,
                                                             const double* nominal, int nobs, const double* obstacles,
                                                             const uint64_t* masks, double* cmds, int32_t* infeasible,
                                                             int32_t* coincident, int smem_group) {
-    constexpr int MAXPAIR = LaneCfg<L>::kMaxPair;
-    constexpr int MAXOBS = MRSIM_MAX_SLOTS / 2;
+    constexpr int MP = LaneCfg<L>::kMaxPair;
+    constexpr int MO = MRSIM_MAX_SLOTS;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const Group<L> g;
+    const Grp<L> g;
     const int lane = g.lane;
     const int gib = threadIdx.x / L;
-    const long long t = static_cast<long long>(blockIdx.x) * (blockDim.x / L) + gib;
-    if (t >= count) return;
+    const long long t_real = static_cast<long long>(blockIdx.x) * (blockDim.x / L) + gib;
+    const bool ghost = t_real >= count;
+    const long long t = ghost ? count - 1 : t_real;
     const int n = 2 * N, P = N * (N - 1) / 2;
-    QpSmem<Real> ws;
+    QpWs<Real> ws;
     Real* wr = reinterpret_cast<Real*>(smem_raw + gib * smem_group);
-    ws.carve(wr, reinterpret_cast<int*>(wr + QpSmem<Real>::reals(n)), n);
-    const bool vlane = lane < n;
-    const int ri = vlane ? lane >> 1 : 0;
-    const int ax = lane & 1;
+    ws.carve(wr, reinterpret_cast<int*>(wr + QpWs<Real>::reals(n)), n);
+    const bool vl = lane < N;
+    const int ri = vl ? lane : 0;
     const double* ps = poses + t * N * 3;
     const double* nm = nominal + t * N * 2;
-    Real x = 0, y = 0, th = 0, nv = 0, nw = 0;
-    if (vlane) {
-        x = Real(ps[3 * ri]);
-        y = Real(ps[3 * ri + 1]);
-        th = Real(ps[3 * ri + 2]);
-        nv = dclamp(Real(nm[2 * ri]), -k.v_max, k.v_max);  // clamp_command (barrier.hpp:142)
-        nw = dclamp(Real(nm[2 * ri + 1]), -k.w_max, k.w_max);
-    }
+    const Real x = Real(ps[3 * ri]), y = Real(ps[3 * ri + 1]), th = Real(ps[3 * ri + 2]);
+    const Real nv = dclamp(Real(nm[2 * ri]), -k.v_max, k.v_max);  // clamp_command (barrier.hpp:142)
+    const Real nw = dclamp(Real(nm[2 * ri + 1]), -k.w_max, k.w_max);
     Real cv = nv, cw = nw;
     int status = kQpOptimal;
     if (c.barrier_enabled) {
-        BarrierRows<Real, L, MAXPAIR, MAXOBS> rows;
-        rows.N = N;
-        rows.n = n;
-        rows.P = P;
-        rows.off_obs = P + 4 * N;
-        rows.off_box = rows.off_obs + N * MRSIM_MAX_SLOTS;
-        rows.cap = k.cap;
-#pragma unroll
-        for (int s = 0; s < MAXPAIR; ++s) {
-            const int pidx = lane + s * L;
-            int i = 0, j = 0;
-            if (pidx < P) pair_of(pidx, N, i, j);
-            rows.pi[s] = i;
-            rows.pj[s] = j;
-        }
+        BarrierRows<Real, L, MP, MO> rows;
+        init_rows(rows, lane, N, k.cap);
         // static obstacles with masks (barrier.hpp:106-119), radius inflated (barrier.hpp:157)
-        rows.nob = 0;
         int obs_rows = 0;
         const double infl = c.projection_distance + c.discrete_margin;
         for (int o = 0; o < nobs; ++o) {
@@ -125,11 +119,11 @@ __global__ void __launch_bounds__(256) barrier_batch_kernel(const __grid_constan
             for (int i = 0; i < N; ++i) {
                 if (mk != 0 && ((mk >> i) & 1ull) == 0) continue;
                 ++obs_rows;
-                if (vlane && i == ri && (o & 1) == ax) {
+                if (vl && i == ri) {
                     const double* ob = obstacles + (t * nobs + o) * 3;
                     const double r = ob[2] + infl;
 #pragma unroll
-                    for (int q = 0; q < MAXOBS; ++q)
+                    for (int q = 0; q < MO; ++q)
                         if (q == rows.nob) {
                             rows.oslot[q] = o;
                             rows.ocx[q] = Real(ob[0]);
@@ -143,16 +137,18 @@ __global__ void __launch_bounds__(256) barrier_batch_kernel(const __grid_constan
         Real sn, cs;
         dsincos(th, &sn, &cs);
         const Real prx = x + cs * k.l, pry = y + sn * k.l;
-        status = barrier_filter<Real, L>(g, rows, ws, k, n, P, vlane, ax, ri, prx, pry, cs, sn, nv, nw,
-                                         P + 4 * N + obs_rows + 2 * n, cv, cw);
+        status = barrier_filter<Real, L>(g, rows, ws, k, !ghost, prx, pry, cs, sn, nv, nw, P + 8 * N + obs_rows, cv,
+                                         cw);
     }
-    if (vlane && ax == 0) {
-        cmds[(t * N + ri) * 2] = double(cv);
-        cmds[(t * N + ri) * 2 + 1] = double(cw);
-    }
-    if (lane == 0) {
-        infeasible[t] = status == kQpInfeasible ? 1 : 0;
-        coincident[t] = status < 0 ? 1 : 0;
+    if (!ghost) {
+        if (vl) {
+            cmds[(t * N + ri) * 2] = double(cv);
+            cmds[(t * N + ri) * 2 + 1] = double(cw);
+        }
+        if (lane == 0) {
+            infeasible[t] = status == kQpInfeasible ? 1 : 0;
+            coincident[t] = status < 0 ? 1 : 0;
+        }
     }
 }
 
@@ -194,10 +190,10 @@ cudaError_t run_barrier(const mrsim_cfg& c, int count, const double* dp, const d
     mrsim_dev::PhysConsts<Real> k;
     mrsim_host::fill_consts(c, k);
     const int N = c.num_robots;
-    const int block = 256;
+    const int block = 128;
     const int gpb = block / L;
-    const int sg = ((mrsim_dev::QpSmem<Real>::reals(2 * N) * static_cast<int>(sizeof(Real)) +
-                     mrsim_dev::QpSmem<Real>::ints(2 * N) * 4) + 15) & ~15;
+    const int sg = ((mrsim_dev::QpWs<Real>::reals(2 * N) * static_cast<int>(sizeof(Real)) +
+                     mrsim_dev::QpWs<Real>::ints(2 * N) * 4) + 15) & ~15;
     const int grid = (count + gpb - 1) / gpb;
     auto kern = mrsim_dev::barrier_batch_kernel<Real, L>;
     if (sg * gpb > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sg * gpb);
@@ -256,13 +252,21 @@ int mrsim_qp_solve_batch(int device, int fp64, int count, int n, int m, const do
     if ((e = upload<double>(dout, nullptr, static_cast<size_t>(count) * n)) != cudaSuccess) return MRSIM_E_CUDA;
     if ((e = upload<int32_t>(dst, nullptr, count)) != cudaSuccess) return MRSIM_E_CUDA;
     if ((e = upload<int32_t>(dit, nullptr, count)) != cudaSuccess) return MRSIM_E_CUDA;
+    const size_t smem_d = 2 * (static_cast<size_t>(m) * n + m + 3 * n + mrsim_dev::QpWs<double>::reals(n)) * 8 + 2 * n * 4;
+    const size_t smem_f = 2 * (static_cast<size_t>(m) * n + m + 3 * n + mrsim_dev::QpWs<float>::reals(n)) * 4 + 2 * n * 4;
+    if (smem_d > 48 * 1024)
+        cudaFuncSetAttribute(mrsim_dev::qp_batch_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem_d));
+    if (smem_f > 48 * 1024)
+        cudaFuncSetAttribute(mrsim_dev::qp_batch_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem_f));
     if (fp64)
-        mrsim_dev::qp_batch_kernel<double><<<count, 32>>>(
+        mrsim_dev::qp_batch_kernel<double><<<(count + 1) / 2, 32, smem_d>>>(
             count, n, m, static_cast<double*>(dA.p), static_cast<double*>(db.p), static_cast<double*>(dlo.p),
             static_cast<double*>(dhi.p), static_cast<double*>(du.p), tolerance, static_cast<double*>(dout.p),
             static_cast<int32_t*>(dst.p), static_cast<int32_t*>(dit.p));
     else
-        mrsim_dev::qp_batch_kernel<float><<<count, 32>>>(
+        mrsim_dev::qp_batch_kernel<float><<<(count + 1) / 2, 32, smem_f>>>(
             count, n, m, static_cast<double*>(dA.p), static_cast<double*>(db.p), static_cast<double*>(dlo.p),
             static_cast<double*>(dhi.p), static_cast<double*>(du.p), tolerance, static_cast<double*>(dout.p),
             static_cast<int32_t*>(dst.p), static_cast<int32_t*>(dit.p));
@@ -296,15 +300,14 @@ int mrsim_apply_barrier_batch(int device, int fp64, const mrsim_cfg* cfg, int co
     int32_t* I_ = static_cast<int32_t*>(di.p);
     int32_t* X_ = static_cast<int32_t*>(dco.p);
     cudaError_t e;
-    const int n = 2 * N;
     if (fp64) {
-        if (n <= 8) e = run_barrier<double, 8>(*cfg, count, P_, N_, num_obstacles, O_, M_, C_, I_, X_);
-        else if (n <= 16) e = run_barrier<double, 16>(*cfg, count, P_, N_, num_obstacles, O_, M_, C_, I_, X_);
-        else e = run_barrier<double, 32>(*cfg, count, P_, N_, num_obstacles, O_, M_, C_, I_, X_);
+        if (N <= 4) e = run_barrier<double, 4>(*cfg, count, P_, N_, num_obstacles, O_, M_, C_, I_, X_);
+        else if (N <= 8) e = run_barrier<double, 8>(*cfg, count, P_, N_, num_obstacles, O_, M_, C_, I_, X_);
+        else e = run_barrier<double, 16>(*cfg, count, P_, N_, num_obstacles, O_, M_, C_, I_, X_);
     } else {
-        if (n <= 8) e = run_barrier<float, 8>(*cfg, count, P_, N_, num_obstacles, O_, M_, C_, I_, X_);
-        else if (n <= 16) e = run_barrier<float, 16>(*cfg, count, P_, N_, num_obstacles, O_, M_, C_, I_, X_);
-        else e = run_barrier<float, 32>(*cfg, count, P_, N_, num_obstacles, O_, M_, C_, I_, X_);
+        if (N <= 4) e = run_barrier<float, 4>(*cfg, count, P_, N_, num_obstacles, O_, M_, C_, I_, X_);
+        else if (N <= 8) e = run_barrier<float, 8>(*cfg, count, P_, N_, num_obstacles, O_, M_, C_, I_, X_);
+        else e = run_barrier<float, 16>(*cfg, count, P_, N_, num_obstacles, O_, M_, C_, I_, X_);
     }
     if (e != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) return MRSIM_E_CUDA;
     std::vector<int32_t> co(count);
