@@ -11,7 +11,7 @@ import os
 from . import _abi
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmrsim_cuda.so")
+LIB_PATH = os.environ.get("MRSIM_LIB_PATH") or os.path.join(_HERE, "libmrsim_cuda.so")  # override: A/B builds
 
 _lib = None
 

@@ -24,6 +24,7 @@ struct mrsim_ctx {
     unsigned flags = 0;
     bool fp64 = false;
     int N = 0, n = 0, P = 0, D = 0, bdim = 0, nf = 0, ni = 0, L = 8;
+    mrsim_host::Variant var{4, 2, 0};
     void* mem[2] = {nullptr, nullptr};
     DevState<float> sf[2];
     DevState<double> sd[2];
@@ -112,32 +113,32 @@ void carve_state(void* base, long long B, int N, int nf, int ni, DevState<Real>&
 
 // ---- dispatch tables over the task template parameter ----
 template <class Real>
-cudaError_t dispatch_step(int task, const StepParams<Real>& p, int L, int grid, int block, int smem,
+cudaError_t dispatch_step(int task, const StepParams<Real>& p, mrsim_host::Variant v, int grid, int block, int smem,
                           cudaStream_t s) {
     using namespace mrsim_host;
     switch (task) {
-        case 0: return launch_step<Real, 0>(p, L, grid, block, smem, s);
-        case 1: return launch_step<Real, 1>(p, L, grid, block, smem, s);
-        case 2: return launch_step<Real, 2>(p, L, grid, block, smem, s);
-        case 3: return launch_step<Real, 3>(p, L, grid, block, smem, s);
-        case 4: return launch_step<Real, 4>(p, L, grid, block, smem, s);
-        case 5: return launch_step<Real, 5>(p, L, grid, block, smem, s);
-        case 6: return launch_step<Real, 6>(p, L, grid, block, smem, s);
-        default: return launch_step<Real, 7>(p, L, grid, block, smem, s);
+        case 0: return launch_step<Real, 0>(p, v, grid, block, smem, s);
+        case 1: return launch_step<Real, 1>(p, v, grid, block, smem, s);
+        case 2: return launch_step<Real, 2>(p, v, grid, block, smem, s);
+        case 3: return launch_step<Real, 3>(p, v, grid, block, smem, s);
+        case 4: return launch_step<Real, 4>(p, v, grid, block, smem, s);
+        case 5: return launch_step<Real, 5>(p, v, grid, block, smem, s);
+        case 6: return launch_step<Real, 6>(p, v, grid, block, smem, s);
+        default: return launch_step<Real, 7>(p, v, grid, block, smem, s);
     }
 }
 template <class Real>
-cudaError_t dispatch_occ(int task, int L, int block, int smem, int* bps) {
+cudaError_t dispatch_occ(int task, mrsim_host::Variant v, int block, int smem, int* bps) {
     using namespace mrsim_host;
     switch (task) {
-        case 0: return step_occupancy<Real, 0>(L, block, smem, bps);
-        case 1: return step_occupancy<Real, 1>(L, block, smem, bps);
-        case 2: return step_occupancy<Real, 2>(L, block, smem, bps);
-        case 3: return step_occupancy<Real, 3>(L, block, smem, bps);
-        case 4: return step_occupancy<Real, 4>(L, block, smem, bps);
-        case 5: return step_occupancy<Real, 5>(L, block, smem, bps);
-        case 6: return step_occupancy<Real, 6>(L, block, smem, bps);
-        default: return step_occupancy<Real, 7>(L, block, smem, bps);
+        case 0: return step_occupancy<Real, 0>(v, block, smem, bps);
+        case 1: return step_occupancy<Real, 1>(v, block, smem, bps);
+        case 2: return step_occupancy<Real, 2>(v, block, smem, bps);
+        case 3: return step_occupancy<Real, 3>(v, block, smem, bps);
+        case 4: return step_occupancy<Real, 4>(v, block, smem, bps);
+        case 5: return step_occupancy<Real, 5>(v, block, smem, bps);
+        case 6: return step_occupancy<Real, 6>(v, block, smem, bps);
+        default: return step_occupancy<Real, 7>(v, block, smem, bps);
     }
 }
 template <class Real>
@@ -255,7 +256,7 @@ int do_step(mrsim_ctx* ctx, DevState<Real>* s, const int8_t* actions, float* obs
     p.smem_bytes_per_group = ctx->smem_group;
     mrsim_host::fill_consts(ctx->cfg, p.k);
     const int smem = ctx->smem_group * (ctx->block / ctx->L);
-    cudaError_t e = dispatch_step<Real>(ctx->cfg.task, p, ctx->L, ctx->grid, ctx->block, smem, stream);
+    cudaError_t e = dispatch_step<Real>(ctx->cfg.task, p, ctx->var, ctx->grid, ctx->block, smem, stream);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "step kernel launch");
     ctx->hist_in[ctx->serial % 64] = ctx->cur;
     ctx->serial += 1;
@@ -530,7 +531,8 @@ int mrsim_create(const mrsim_cfg* cfg, int device, int64_t num_envs, uint32_t fl
     ctx->D = mrsim_dev::obs_dim_of(*cfg);
     ctx->bdim = mrsim_dev::base_obs_dim(*cfg);
     mrsim_dev::task_fields(*cfg, &ctx->nf, &ctx->ni);
-    ctx->L = ctx->N <= 4 ? 4 : (ctx->N <= 8 ? 8 : 16);  // lane per robot
+    ctx->var = mrsim_host::pick_variant(*cfg);  // lane per robot
+    ctx->L = ctx->var.L;
     cudaError_t e = cudaSetDevice(device);
     if (e != cudaSuccess) {
         rc = cuda_fail(ctx, e, "cudaSetDevice");
@@ -584,8 +586,8 @@ int mrsim_create(const mrsim_cfg* cfg, int device, int64_t num_envs, uint32_t fl
                                 : mrsim_dev::GroupSmem<float>::bytes(ctx->N, ctx->nf, ctx->ni);
     const int smem = ctx->smem_group * (ctx->block / ctx->L);
     int bps = 0;
-    e = ctx->fp64 ? dispatch_occ<double>(cfg->task, ctx->L, ctx->block, smem, &bps)
-                  : dispatch_occ<float>(cfg->task, ctx->L, ctx->block, smem, &bps);
+    e = ctx->fp64 ? dispatch_occ<double>(cfg->task, ctx->var, ctx->block, smem, &bps)
+                  : dispatch_occ<float>(cfg->task, ctx->var, ctx->block, smem, &bps);
     if (e != cudaSuccess) return bail(e, "occupancy query");
     if (bps < 1) bps = 1;
     const long long gpb = ctx->block / ctx->L;

@@ -35,11 +35,28 @@ inline void fill_consts(const mrsim_cfg& c, mrsim_dev::PhysConsts<Real>& k) {
     k.tol = mrsim_dev::Prec<Real>::tol;
 }
 
+// Kernel variant for a config: L lanes per env (lane per robot), MP pair-row
+// slots per lane, MO obstacle-row slots per lane (rware only).
+struct Variant {
+    int L, MP, MO;
+};
+inline Variant pick_variant(const mrsim_cfg& c) {
+    const int N = c.num_robots, P = N * (N - 1) / 2;
+    Variant v;
+    v.L = N <= 4 ? 4 : (N <= 8 ? 8 : 16);
+    const int need = (P + v.L - 1) / v.L;
+    if (v.L == 4) v.MP = 2;
+    else if (v.L == 8) v.MP = need <= 2 ? 2 : 4;
+    else v.MP = need <= 3 ? 3 : 8;
+    v.MO = c.task == MRSIM_TASK_RWARE ? (c.layout.rware_num_slots <= 6 ? 6 : 16) : 0;
+    return v;
+}
+
 template <class Real, int TASK>
-cudaError_t launch_step(const mrsim_dev::StepParams<Real>& p, int L, int grid, int block, int smem,
+cudaError_t launch_step(const mrsim_dev::StepParams<Real>& p, Variant v, int grid, int block, int smem,
                         cudaStream_t stream);
 template <class Real, int TASK>
-cudaError_t step_occupancy(int L, int block, int smem, int* blocks_per_sm);
+cudaError_t step_occupancy(Variant v, int block, int smem, int* blocks_per_sm);
 template <class Real, int TASK>
 cudaError_t launch_observe(const mrsim_cfg& c, const mrsim_dev::DevState<Real>& s, float* obs, long long B, int D,
                            int bdim, int nf, int ni, cudaStream_t stream);

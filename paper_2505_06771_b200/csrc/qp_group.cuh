@@ -33,22 +33,28 @@ enum QpStatusDev : int { kQpOptimal = 0, kQpInfeasible = 1, kQpIterLimit = 2 };
 
 // Shared-memory workspace of one group for n variables:
 //   Q[a*n + v] (column a = active slot a), R[col*n + row] (upper triangular),
-//   gS (entering normal), cS (Q^T g), rS (R^{-1} c), lamS (multipliers), act (row ids)
+//   Rd[a] = 1 / R[a][a], gS (entering normal), cS (Q^T g).
+// Per-slot scalars (c_a, r_a, lambda_a, row id) live in registers of lane
+// a % L (slots a = lane and a = lane + L; k <= n = 2N <= 2L).
 template <class Real>
 struct QpWs {
-    Real *Q, *R, *gS, *cS, *rS, *lamS;
-    int* act;
-    static __host__ __device__ constexpr int reals(int n) { return 2 * n * n + 4 * n; }
-    static __host__ __device__ constexpr int ints(int n) { return n; }
-    __device__ void carve(Real* base, int* ibase, int n) {
+    Real *Q, *R, *Rd, *gS, *cS;
+    static __host__ __device__ constexpr int reals(int n) { return 2 * n * n + 3 * n; }
+    static __host__ __device__ constexpr int ints(int) { return 0; }
+    __device__ void carve(Real* base, int*, int n) {
         Q = base;
         R = Q + n * n;
-        gS = R + n * n;
+        Rd = R + n * n;
+        gS = Rd + n;
         cS = gS + n;
-        rS = cS + n;
-        lamS = rS + n;
-        act = ibase;
     }
+};
+
+// Slot registers of one lane: slots a0 = lane, a1 = lane + L.
+template <class Real>
+struct Slots {
+    Real c0, c1, r0, r1, lam0, lam1;
+    int act0, act1;
 };
 
 // Drop active slot `bi` of the groups with do_drop set (the reference erases
@@ -56,21 +62,31 @@ struct QpWs {
 // delete column bi of R and restore triangularity with Givens rotations that
 // are applied to Q's columns as well. Order of the remaining slots is kept.
 template <class Real, int L, class RowSet>
-__device__ __forceinline__ void qp_drop(const Grp<L>& g, RowSet& rows, const QpWs<Real>& ws, int n, int& k,
-                                        bool do_drop, int bi) {
+__device__ __forceinline__ void qp_drop(const Grp<L>& g, RowSet& rows, const QpWs<Real>& ws, Slots<Real>& sl, int n,
+                                        int& k, bool do_drop, int bi) {
     const int lane = g.lane;
-    if (do_drop) rows.set_active(g, ws.act[bi], false);
-    Real tl0 = 0, tl1 = 0;
-    int ta0 = 0, ta1 = 0;
     const int a0 = lane, a1 = lane + L;
-    const bool m0 = do_drop && a0 >= bi && a0 < k - 1;
-    const bool m1 = do_drop && a1 >= bi && a1 < k - 1;
-    if (m0) { tl0 = ws.lamS[a0 + 1]; ta0 = ws.act[a0 + 1]; }
-    if (m1) { tl1 = ws.lamS[a1 + 1]; ta1 = ws.act[a1 + 1]; }
-    Grp<L>::sync();
-    if (m0) { ws.lamS[a0] = tl0; ws.act[a0] = ta0; }
-    if (m1) { ws.lamS[a1] = tl1; ws.act[a1] = ta1; }
-    if (do_drop) {  // delete column bi of R (lane = rows lane, lane+L)
+    // clear the dropped row's active bit (row id lives on lane bi % L)
+    const int bsrc = bi < 0 ? 0 : (bi & (L - 1));
+    const int dr0 = g.shfl(sl.act0, bsrc), dr1 = g.shfl(sl.act1, bsrc);  // both unconditionally (lockstep)
+    const int drop_row = (bi >= L) ? dr1 : dr0;
+    if (do_drop) rows.set_active(g, drop_row, false);
+    // shift slots (bi, k) down by one: slot a takes slot a+1
+    const int nxt = (lane + 1) & (L - 1);
+    const Real l0n = g.shfl(sl.lam0, nxt), l1n = g.shfl(sl.lam1, nxt);
+    const int c0n = g.shfl(sl.act0, nxt), c1n = g.shfl(sl.act1, nxt);
+    const Real l1_from0 = g.shfl(sl.lam1, 0);
+    const int c1_from0 = g.shfl(sl.act1, 0);
+    if (do_drop) {
+        if (a0 >= bi && a0 < k - 1) {
+            sl.lam0 = (lane < L - 1) ? l0n : l1_from0;
+            sl.act0 = (lane < L - 1) ? c0n : c1_from0;
+        }
+        if (a1 >= bi && a1 < k - 1) {
+            sl.lam1 = l1n;
+            sl.act1 = c1n;
+        }
+        // delete column bi of R (this lane's rows)
         for (int row = lane; row < k; row += L)
             for (int col = bi; col < k - 1; ++col) ws.R[col * n + row] = ws.R[(col + 1) * n + row];
     }
@@ -93,20 +109,22 @@ __device__ __forceinline__ void qp_drop(const Grp<L>& g, RowSet& rows, const QpW
                 ws.R[col * n + j] = cg * x + sg * y;
                 ws.R[col * n + j + 1] = (col == j) ? Real(0) : (-sg * x + cg * y);
             }
-            if (2 * lane < n) {
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int v = 2 * lane + h;
-                    if (v >= n) continue;
-                    const Real x = ws.Q[j * n + v], y = ws.Q[(j + 1) * n + v];
-                    ws.Q[j * n + v] = cg * x + sg * y;
-                    ws.Q[(j + 1) * n + v] = -sg * x + cg * y;
-                }
+            for (int h = 0; h < 2; ++h) {
+                const int v = 2 * lane + h;
+                if (v >= n) continue;
+                const Real x = ws.Q[j * n + v], y = ws.Q[(j + 1) * n + v];
+                ws.Q[j * n + v] = cg * x + sg * y;
+                ws.Q[(j + 1) * n + v] = -sg * x + cg * y;
             }
         }
         Grp<L>::sync();
     }
-    if (do_drop) --k;
+    if (do_drop) {
+        --k;
+        for (int a = lane; a < k; a += L)
+            if (a >= bi) ws.Rd[a] = Real(1) / ws.R[a * n + a];
+    }
 }
 
 // Solve for the groups with `participate` set. (ux, uy): this lane's pair of
@@ -117,6 +135,8 @@ __device__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpWs<Real>& ws, int
     const int lane = g.lane;
     const bool vl = 2 * lane < n;      // this lane's x variable exists
     const bool vly = 2 * lane + 1 < n;  // ... and its y variable (n may be odd for dense QPs)
+    const int a0 = lane, a1 = lane + L;
+    Slots<Real> sl{0, 0, 0, 0, 0, 0, 0, 0};
     int k = 0;
     int status = kQpOptimal;
     bool done = !participate;
@@ -133,6 +153,7 @@ __device__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpWs<Real>& ws, int
         rows.scan(g, ux, uy, worst, p);
         g.argmax(worst, p);
         if (!done && p < 0) done = true;
+        if (!Grp<L>::warp_any(!done)) break;  // every env of the warp is optimal
         bool act = !done;
         Real gx, gy, hp;
         rows.fetch(g, act ? p : rows.dummy_row(), gx, gy, hp);
@@ -152,13 +173,20 @@ __device__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpWs<Real>& ws, int
         Real lam_p = 0;
         int guard = 0;
         while (Grp<L>::warp_any(in)) {  // qp.hpp:262-330
-            // c = Q^T g (slots of this lane), r <- c
+            // c = Q^T g on this lane's slots
+            sl.c0 = sl.c1 = Real(0);
             if (in) {
-                for (int a = lane; a < k; a += L) {
+                if (a0 < k) {
                     Real c = 0;
-                    for (int v = 0; v < n; ++v) c += ws.Q[a * n + v] * ws.gS[v];
-                    ws.cS[a] = c;
-                    ws.rS[a] = c;
+                    for (int v = 0; v < n; ++v) c += ws.Q[a0 * n + v] * ws.gS[v];
+                    sl.c0 = c;
+                    ws.cS[a0] = c;
+                }
+                if (a1 < k) {
+                    Real c = 0;
+                    for (int v = 0; v < n; ++v) c += ws.Q[a1 * n + v] * ws.gS[v];
+                    sl.c1 = c;
+                    ws.cS[a1] = c;
                 }
             }
             Grp<L>::sync();
@@ -171,17 +199,19 @@ __device__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpWs<Real>& ws, int
                     if (vly) zy -= ws.Q[a * n + 2 * lane + 1] * ca;
                 }
             }
-            // r = R^{-1} c (back substitution, column oriented)
+            // r = R^{-1} c: column-oriented back substitution, r_b broadcast by shuffle
+            sl.r0 = sl.c0;
+            sl.r1 = sl.c1;
             const int kmax = Grp<L>::warp_max(in ? k : 0);
             for (int b = kmax - 1; b >= 0; --b) {
-                const bool on = in && b < k;
-                if (on && lane == (b & (L - 1))) ws.rS[b] = ws.rS[b] / ws.R[b * n + b];
-                Grp<L>::sync();
-                if (on) {
-                    const Real rb = ws.rS[b];
-                    for (int a = lane; a < b; a += L) ws.rS[a] -= ws.R[b * n + a] * rb;
+                const bool hi = b >= L;
+                const Real rb = g.shfl(hi ? sl.r1 : sl.r0, b & (L - 1)) * ws.Rd[b];
+                if (in && b < k) {
+                    if (a0 == b) sl.r0 = rb;
+                    else if (a0 < b) sl.r0 -= ws.R[b * n + a0] * rb;
+                    if (a1 == b) sl.r1 = rb;
+                    else if (a1 < b) sl.r1 -= ws.R[b * n + a1] * rb;
                 }
-                Grp<L>::sync();
             }
             const Real z2 = g.sum(zx * zx + zy * zy);
             const Real viol = g.sum(gx * ux + gy * uy) - hp;  // qp.hpp:281
@@ -189,14 +219,15 @@ __device__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpWs<Real>& ws, int
             Real t1 = Consts<Real>::inf;
             int bi = -1;
             if (in) {
-                for (int a = lane; a < k; a += L) {
-                    const Real ra = ws.rS[a];
-                    if (ra > Prec<Real>::eps_r) {
-                        const Real t = ws.lamS[a] / ra;
-                        if (bi < 0 || t < t1) {
-                            t1 = t;
-                            bi = a;
-                        }
+                if (a0 < k && sl.r0 > Prec<Real>::eps_r) {
+                    t1 = sl.lam0 / sl.r0;
+                    bi = a0;
+                }
+                if (a1 < k && sl.r1 > Prec<Real>::eps_r) {
+                    const Real t = sl.lam1 / sl.r1;
+                    if (bi < 0 || t < t1) {
+                        t1 = t;
+                        bi = a1;
                     }
                 }
             }
@@ -233,25 +264,33 @@ __device__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpWs<Real>& ws, int
                 uy -= t * zy;
             }
             if (step_l) {
-                for (int a = lane; a < k; a += L) ws.lamS[a] -= t * ws.rS[a];
+                if (a0 < k) sl.lam0 -= t * sl.r0;
+                if (a1 < k) sl.lam1 -= t * sl.r1;
                 lam_p += t;
             }
-            Grp<L>::sync();
             if (do_add) {
                 const Real rho = dsqrt(z2);
-                if (vl) ws.Q[k * n + 2 * lane] = zx / rho;
-                if (vly) ws.Q[k * n + 2 * lane + 1] = zy / rho;
-                for (int a = lane; a < k; a += L) ws.R[k * n + a] = ws.cS[a];
+                const Real irho = Real(1) / rho;
+                if (vl) ws.Q[k * n + 2 * lane] = zx * irho;
+                if (vly) ws.Q[k * n + 2 * lane + 1] = zy * irho;
+                if (a0 < k) ws.R[k * n + a0] = sl.c0;
+                if (a1 < k) ws.R[k * n + a1] = sl.c1;
                 if (lane == 0) {
                     ws.R[k * n + k] = rho;
-                    ws.lamS[k] = lam_p;
-                    ws.act[k] = p;
+                    ws.Rd[k] = irho;
+                }
+                if (a0 == k) {
+                    sl.lam0 = lam_p;
+                    sl.act0 = p;
+                }
+                if (a1 == k) {
+                    sl.lam1 = lam_p;
+                    sl.act1 = p;
                 }
                 rows.set_active(g, p, true);
                 ++k;
             }
-            Grp<L>::sync();
-            qp_drop<Real, L>(g, rows, ws, n, k, do_drop, bi);
+            qp_drop<Real, L>(g, rows, ws, sl, n, k, do_drop, bi);
             if (finish) {
                 in = false;
                 added = true;
@@ -263,6 +302,7 @@ __device__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpWs<Real>& ws, int
             }
             ++guard;
             if (in && guard > total_rows) in = false;  // guard exhausted without adding
+            Grp<L>::sync();
         }
         if (act && !added) done = true;  // stall (qp.hpp:331-334) or infeasible
         if (act) ++iter;

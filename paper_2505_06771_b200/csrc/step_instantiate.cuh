@@ -7,10 +7,9 @@
 
 namespace mrsim_host {
 
-template <class Real, int L>
-static cudaError_t launch_L(const mrsim_dev::StepParams<Real>& p, int grid, int block, int smem,
-                            cudaStream_t stream) {
-    auto k = mrsim_dev::step_kernel<Real, L, MRSIM_TASK_ID>;
+template <class Real, int L, int MP, int MO>
+static cudaError_t launch_V(const mrsim_dev::StepParams<Real>& p, int grid, int block, int smem, cudaStream_t stream) {
+    auto k = mrsim_dev::step_kernel<Real, L, MP, MO, MRSIM_TASK_ID>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
@@ -19,9 +18,9 @@ static cudaError_t launch_L(const mrsim_dev::StepParams<Real>& p, int grid, int 
     return cudaGetLastError();
 }
 
-template <class Real, int L>
-static cudaError_t occ_L(int block, int smem, int* bps) {
-    auto k = mrsim_dev::step_kernel<Real, L, MRSIM_TASK_ID>;
+template <class Real, int L, int MP, int MO>
+static cudaError_t occ_V(int block, int smem, int* bps) {
+    auto k = mrsim_dev::step_kernel<Real, L, MP, MO, MRSIM_TASK_ID>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
@@ -29,32 +28,58 @@ static cudaError_t occ_L(int block, int smem, int* bps) {
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k, block, smem);
 }
 
+// The instantiated (L, MP, MO) set; pick_variant (launch.h) maps configs onto it.
+#define MRSIM_VARIANTS(X, MO)  \
+    X(4, 2, MO) X(8, 2, MO) X(8, 4, MO) X(16, 3, MO) X(16, 8, MO)
+
+template <class Real>
+static cudaError_t launch_any(const mrsim_dev::StepParams<Real>& p, Variant v, int grid, int block, int smem,
+                              cudaStream_t s) {
+#define MRSIM_CASE(l, mp, mo) \
+    if (v.L == l && v.MP == mp && v.MO == mo) return launch_V<Real, l, mp, mo>(p, grid, block, smem, s);
+    if constexpr (MRSIM_TASK_ID == MRSIM_TASK_RWARE) {
+        MRSIM_VARIANTS(MRSIM_CASE, 6)
+        MRSIM_VARIANTS(MRSIM_CASE, 16)
+    } else {
+        MRSIM_VARIANTS(MRSIM_CASE, 0)
+    }
+#undef MRSIM_CASE
+    return cudaErrorInvalidValue;
+}
+
+template <class Real>
+static cudaError_t occ_any(Variant v, int block, int smem, int* bps) {
+#define MRSIM_CASE(l, mp, mo) \
+    if (v.L == l && v.MP == mp && v.MO == mo) return occ_V<Real, l, mp, mo>(block, smem, bps);
+    if constexpr (MRSIM_TASK_ID == MRSIM_TASK_RWARE) {
+        MRSIM_VARIANTS(MRSIM_CASE, 6)
+        MRSIM_VARIANTS(MRSIM_CASE, 16)
+    } else {
+        MRSIM_VARIANTS(MRSIM_CASE, 0)
+    }
+#undef MRSIM_CASE
+    return cudaErrorInvalidValue;
+}
+
 template <>
-cudaError_t launch_step<float, MRSIM_TASK_ID>(const mrsim_dev::StepParams<float>& p, int L, int grid, int block,
+cudaError_t launch_step<float, MRSIM_TASK_ID>(const mrsim_dev::StepParams<float>& p, Variant v, int grid, int block,
                                               int smem, cudaStream_t s) {
-    if (L == 4) return launch_L<float, 4>(p, grid, block, smem, s);
-    if (L == 8) return launch_L<float, 8>(p, grid, block, smem, s);
-    return launch_L<float, 16>(p, grid, block, smem, s);
+    return launch_any<float>(p, v, grid, block, smem, s);
 }
 template <>
-cudaError_t launch_step<double, MRSIM_TASK_ID>(const mrsim_dev::StepParams<double>& p, int L, int grid, int block,
-                                               int smem, cudaStream_t s) {
-    if (L == 4) return launch_L<double, 4>(p, grid, block, smem, s);
-    if (L == 8) return launch_L<double, 8>(p, grid, block, smem, s);
-    return launch_L<double, 16>(p, grid, block, smem, s);
+cudaError_t launch_step<double, MRSIM_TASK_ID>(const mrsim_dev::StepParams<double>& p, Variant v, int grid,
+                                               int block, int smem, cudaStream_t s) {
+    return launch_any<double>(p, v, grid, block, smem, s);
 }
 template <>
-cudaError_t step_occupancy<float, MRSIM_TASK_ID>(int L, int block, int smem, int* bps) {
-    if (L == 4) return occ_L<float, 4>(block, smem, bps);
-    if (L == 8) return occ_L<float, 8>(block, smem, bps);
-    return occ_L<float, 16>(block, smem, bps);
+cudaError_t step_occupancy<float, MRSIM_TASK_ID>(Variant v, int block, int smem, int* bps) {
+    return occ_any<float>(v, block, smem, bps);
 }
 template <>
-cudaError_t step_occupancy<double, MRSIM_TASK_ID>(int L, int block, int smem, int* bps) {
-    if (L == 4) return occ_L<double, 4>(block, smem, bps);
-    if (L == 8) return occ_L<double, 8>(block, smem, bps);
-    return occ_L<double, 16>(block, smem, bps);
+cudaError_t step_occupancy<double, MRSIM_TASK_ID>(Variant v, int block, int smem, int* bps) {
+    return occ_any<double>(v, block, smem, bps);
 }
+
 template <>
 cudaError_t launch_observe<float, MRSIM_TASK_ID>(const mrsim_cfg& c, const mrsim_dev::DevState<float>& s, float* obs,
                                                  long long B, int D, int bdim, int nf, int ni, cudaStream_t st) {

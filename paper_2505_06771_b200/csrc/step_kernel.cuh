@@ -20,6 +20,12 @@
 #include "qp_group.cuh"
 #include "tasks.cuh"
 
+// 128-thread blocks per SM the register budget is sized for (measured on B200:
+// 4 -> <=128 regs is best for L <= 8; 3 -> <=168 regs for the QP-heavy L = 16).
+#ifndef MRSIM_MIN_BLOCKS
+#define MRSIM_MIN_BLOCKS(L) ((L) >= 16 ? 3 : 4)
+#endif
+
 namespace mrsim_dev {
 
 // SoA batch state in HBM (one copy; the context ping-pongs two copies so a
@@ -90,8 +96,6 @@ struct LaneCfg {  // pair slots per lane for N <= L robots: ceil(L(L-1)/2 / L)
     static constexpr int kMaxPair = (L * (L - 1) / 2 + L - 1) / L;
 };
 
-template <int TASK>
-struct TaskCfg { static constexpr int kMaxObs = (TASK == MRSIM_TASK_RWARE) ? MRSIM_MAX_SLOTS : 0; };
 
 // ---------------------------------------------------------------------------
 // Barrier rows of one tick (build_barrier_constraints + fold_rows), owned by
@@ -119,8 +123,11 @@ struct BarrierRows {
 
     __device__ __forceinline__ int dummy_row() const { return off_box; }
 
+    // A lane scans its rows in increasing global index, so the reference's
+    // strict `v > worst` (first maximal row wins) is exact within the lane;
+    // the group argmax breaks cross-lane ties toward the lowest index.
     __device__ __forceinline__ static void consider(Real val, int idx, Real& worst, int& p) {
-        if (val > worst || (val == worst && p >= 0 && idx < p)) {
+        if (val > worst) {
             worst = val;
             p = idx;
         }
@@ -147,11 +154,14 @@ struct BarrierRows {
                     if (t < nob && off(MP + 8 + t))
                         consider(ogx[t] * ux + ogy[t] * uy - oh[t], off_obs + lane * MRSIM_MAX_SLOTS + oslot[t], worst, p);
             }
-            const int b0 = off_box + 4 * lane;
-            if (off(MP + 4)) consider(ux - cap, b0, worst, p);
-            if (off(MP + 5)) consider(-ux - cap, b0 + 1, worst, p);
-            if (off(MP + 6)) consider(uy - cap, b0 + 2, worst, p);
-            if (off(MP + 7)) consider(-uy - cap, b0 + 3, worst, p);
+            // box sides (fold_rows qp.hpp:126-139): only reachable when |u| > cap
+            if (dabs(ux) > cap || dabs(uy) > cap) {
+                const int b0 = off_box + 4 * lane;
+                if (off(MP + 4)) consider(ux - cap, b0, worst, p);
+                if (off(MP + 5)) consider(-ux - cap, b0 + 1, worst, p);
+                if (off(MP + 6)) consider(uy - cap, b0 + 2, worst, p);
+                if (off(MP + 7)) consider(-uy - cap, b0 + 3, worst, p);
+            }
         }
     }
 
@@ -292,7 +302,7 @@ __device__ int barrier_filter(const Grp<L>& g, BarrierRows<Real, L, MP, MO>& row
         const Real dist2 = dx * dx + dy * dy;
         if (s < rows.npair && dist2 < Real(1e-18)) coincident = true;
         const Real h = dist2 - k.r_eff2;
-        const Real inv = Real(1) / dsqrt(Real(8) * dist2);
+        const Real inv = rsqrt(Real(8) * dist2);
         rows.pgx[s] = Real(2) * dx * inv;
         rows.pgy[s] = Real(2) * dy * inv;
         rows.ph[s] = k.gamma * h * h * h * inv;
@@ -385,10 +395,8 @@ __device__ __forceinline__ Real wrap_angle_dev(Real t) {
 // The fused step kernel. Persistent grid-stride loop; each warp steps 32/L
 // environments in lockstep (ghost groups past the end compute but never store).
 // ---------------------------------------------------------------------------
-template <class Real, int L, int TASK>
-__global__ void __launch_bounds__(128) step_kernel(const __grid_constant__ StepParams<Real> p) {
-    constexpr int MP = LaneCfg<L>::kMaxPair;
-    constexpr int MO = TaskCfg<TASK>::kMaxObs;
+template <class Real, int L, int MP, int MO, int TASK>
+__global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L)) step_kernel(const __grid_constant__ StepParams<Real> p) {
     constexpr int G = 32 / L;  // envs per warp
     if (*p.err != ~0ull) return;  // sticky device error: later steps are no-ops
 
@@ -533,16 +541,16 @@ __global__ void __launch_bounds__(128) step_kernel(const __grid_constant__ StepP
             x = dclamp(x, -p.k.hw, p.k.hw);
             y = dclamp(y, -p.k.hh, p.k.hh);
             // collision check (batch.hpp:204-209)
-            if (N > 1) {
-                Real md = Consts<Real>::inf;
+            if (N > 1) {  // min over pairs of squared distances; sqrt is monotone
+                Real md2 = Consts<Real>::inf;
 #pragma unroll
                 for (int s = 0; s < MP; ++s) {
                     const Real xi = g.shfl(x, rows.pi[s]), yi = g.shfl(y, rows.pi[s]);
                     const Real xj = g.shfl(x, rows.pj[s]), yj = g.shfl(y, rows.pj[s]);
                     const Real dx = xi - xj, dy = yi - yj;
-                    if (s < rows.npair) md = dmin(md, dsqrt(dx * dx + dy * dy));
+                    if (s < rows.npair) md2 = dmin(md2, dx * dx + dy * dy);
                 }
-                md = g.min(md);
+                const Real md = dsqrt(g.min(md2));
                 min_dist = dmin(min_dist, md);
                 collision = collision || md < p.k.coll_r;
             }

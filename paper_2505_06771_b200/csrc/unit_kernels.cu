@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(128) barrier_batch_kernel(const __grid_constan
                                                             const double* nominal, int nobs, const double* obstacles,
                                                             const uint64_t* masks, double* cmds, int32_t* infeasible,
                                                             int32_t* coincident, int smem_group) {
-    constexpr int MP = LaneCfg<L>::kMaxPair;
+    constexpr int MP = LaneCfg<L>::kMaxPair;  // any N <= L
     constexpr int MO = MRSIM_MAX_SLOTS;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Grp<L> g;
