@@ -18,6 +18,7 @@ inline void fill_consts(const mrsim_cfg& c, mrsim_dev::PhysConsts<Real>& k) {
     k.hw = Real(c.arena_half_width);
     k.hh = Real(c.arena_half_height);
     k.coll_r = Real(c.collision_radius);
+    k.coll_r2 = Real(c.collision_radius * c.collision_radius);
     k.k_pos = Real(c.k_position);
     k.l = Real(l);
     k.inv_l = Real(1.0 / l);

@@ -172,6 +172,38 @@ __device__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpWs<Real>& ws, int
         bool in = act, added = false;
         Real lam_p = 0;
         int guard = 0;
+        if (__all_sync(Grp<L>::kFull, !act || k == 0)) {
+            // Every active group enters its first row: the inner loop of
+            // qp.hpp:262-330 with an empty active set, specialised (c = r = 0,
+            // z = g, t1 = inf). Same arithmetic as the general path.
+            const Real z2 = gn;  // same reduction as the general path's |z|^2 with z = g
+            const Real viol = g.sum(gx * ux + gy * uy) - hp;
+            if (act) {
+                if (viol > tol && z2 > Prec<Real>::eps_z) {
+                    const Real t = viol / z2;  // t = min(inf, t2)
+                    ux -= t * gx;
+                    uy -= t * gy;
+                    const Real rho = dsqrt(z2);
+                    const Real irho = Real(1) / rho;
+                    if (vl) ws.Q[2 * lane] = gx * irho;
+                    if (vly) ws.Q[2 * lane + 1] = gy * irho;
+                    if (lane == 0) {
+                        ws.R[0] = rho;
+                        ws.Rd[0] = irho;
+                        sl.lam0 = t;
+                        sl.act0 = p;
+                    }
+                    rows.set_active(g, p, true);
+                    k = 1;
+                } else if (viol > tol) {  // dependent normal, nothing blocks: infeasible (qp.hpp:304-309)
+                    status = kQpInfeasible;
+                    done = true;
+                }
+                added = true;  // (viol <= tol: finished without adding, lam_p == 0)
+            }
+            Grp<L>::sync();
+            in = false;
+        }
         while (Grp<L>::warp_any(in)) {  // qp.hpp:262-330
             // c = Q^T g on this lane's slots
             sl.c0 = sl.c1 = Real(0);
@@ -182,7 +214,7 @@ __device__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpWs<Real>& ws, int
                     sl.c0 = c;
                     ws.cS[a0] = c;
                 }
-                if (a1 < k) {
+                if (a1 < k) {  // (slots >= L only exist for N > L/2 ... k > L)
                     Real c = 0;
                     for (int v = 0; v < n; ++v) c += ws.Q[a1 * n + v] * ws.gS[v];
                     sl.c1 = c;

@@ -53,7 +53,7 @@ struct EnvStats {
 // inflation of apply_barrier (barrier.hpp:151-157, 173).
 template <class Real>
 struct PhysConsts {
-    Real dt, v_max, w_max, si_max, hw, hh, coll_r, k_pos, l, inv_l, gamma, r_eff2, cap, obs_r_eff2, tol;
+    Real dt, v_max, w_max, si_max, hw, hh, coll_r, coll_r2, k_pos, l, inv_l, gamma, r_eff2, cap, obs_r_eff2, tol;
     Real wall_xmin, wall_xmax, wall_ymin, wall_ymax;
 };
 
@@ -357,11 +357,11 @@ template <class Real>
 struct GroupSmem {
     QpWs<Real> qp;
     Real *xs, *ys, *ts, *tf;
-    int *ti, *misc;
+    int *ti, *misc, *drones;
     static __host__ __device__ int bytes(int N, int nf, int ni) {
         const int n = 2 * N;
         const int reals = QpWs<Real>::reals(n) + 3 * N + nf;
-        const int ints = QpWs<Real>::ints(n) + ni + 2;
+        const int ints = QpWs<Real>::ints(n) + ni + 2 + N;
         const int b = reals * static_cast<int>(sizeof(Real)) + ints * 4;
         return (b + 15) & ~15;
     }
@@ -376,6 +376,7 @@ struct GroupSmem {
         tf = ts + N;
         ti = ib + QpWs<Real>::ints(n);
         misc = ti;  // misc words follow the ni task words (set by the kernel)
+        drones = nullptr;
     }
 };
 
@@ -410,6 +411,8 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L)) step_kernel(const __
     GroupSmem<Real> sm;
     sm.carve(smem_raw + gib * p.smem_bytes_per_group, N, p.nf);
     int* misc = sm.ti + p.ni;
+    sm.drones = misc + 2;
+    if (TASK == MRSIM_TASK_ARCTIC_TRANSPORT && lane == 0) arctic_drones(c, sm.drones);
 
     const bool vl = lane < N;  // lane r carries robot r
     const int ri = vl ? lane : 0;
@@ -417,7 +420,7 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L)) step_kernel(const __
     BarrierRows<Real, L, MP, MO> rows;
     init_rows(rows, lane, N, p.k.cap);
     const int total_rows_base = rows.P + 4 * N + 4 * N;
-    const EnvView<Real> view{sm.xs, sm.ys, sm.ts, sm.tf, sm.ti, N};
+    const EnvView<Real> view{sm.xs, sm.ys, sm.ts, sm.tf, sm.ti, N, sm.drones};
     const long long stride = static_cast<long long>(gridDim.x) * gpb;
 
     for (long long e0 = static_cast<long long>(blockIdx.x) * gpb + (gib & ~(G - 1)); e0 < p.B; e0 += stride) {
@@ -495,6 +498,7 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L)) step_kernel(const __
 
         // ---- physics ticks ----
         Real min_dist = p.in.min_dist[e];
+        Real min_d2 = Consts<Real>::inf;  // min squared pairwise distance over this step's ticks
         int qp_inf = p.in.qp_inf[e];
         bool collision = false;
         for (int tick = 0; tick < c.sub_steps; ++tick) {
@@ -541,7 +545,7 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L)) step_kernel(const __
             x = dclamp(x, -p.k.hw, p.k.hw);
             y = dclamp(y, -p.k.hh, p.k.hh);
             // collision check (batch.hpp:204-209)
-            if (N > 1) {  // min over pairs of squared distances; sqrt is monotone
+            if (N > 1) {  // squared distances; sqrt is monotone, so it is taken once per step
                 Real md2 = Consts<Real>::inf;
 #pragma unroll
                 for (int s = 0; s < MP; ++s) {
@@ -550,12 +554,13 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L)) step_kernel(const __
                     const Real dx = xi - xj, dy = yi - yj;
                     if (s < rows.npair) md2 = dmin(md2, dx * dx + dy * dy);
                 }
-                const Real md = dsqrt(g.min(md2));
-                min_dist = dmin(min_dist, md);
-                collision = collision || md < p.k.coll_r;
+                md2 = g.min(md2);
+                min_d2 = dmin(min_d2, md2);
+                collision = collision || md2 < p.k.coll_r2;
             }
         }
 
+        min_dist = dmin(min_dist, dsqrt(min_d2));
         // ---- stage final poses, transition, bookkeeping (lane 0) ----
         if (vl) {
             sm.xs[ri] = x;
@@ -738,7 +743,9 @@ __global__ void __launch_bounds__(128) reset_kernel(const __grid_constant__ Rese
     p.out.min_dist[e] = Consts<Real>::inf;
     p.out.ep_return[e] = 0;
     if (p.obs) {
-        const EnvView<Real> v{xs, ys, ts, tf, ro.ti, N};
+        int drones[MRSIM_MAX_ROBOTS];
+        arctic_drones(c, drones);
+        const EnvView<Real> v{xs, ys, ts, tf, ro.ti, N, drones};
         float* o = p.obs + e * N * p.D;
         for (int r = 0; r < N; ++r)
             for (int q = 0; q < p.D; ++q) o[r * p.D + q] = obs_feature<TASK, Real>(c, v, r, q, p.bdim);
@@ -760,7 +767,9 @@ __global__ void __launch_bounds__(128) observe_kernel(const __grid_constant__ mr
     }
     for (int f = 0; f < nf; ++f) tf[f] = s.tf[static_cast<long long>(f) * B + e];
     for (int w = 0; w < ni; ++w) ti[w] = s.ti[static_cast<long long>(w) * B + e];
-    const EnvView<Real> v{xs, ys, ts, tf, ti, N};
+    int drones[MRSIM_MAX_ROBOTS];
+    arctic_drones(c, drones);
+    const EnvView<Real> v{xs, ys, ts, tf, ti, N, drones};
     float* o = obs + e * N * D;
     for (int r = 0; r < N; ++r)
         for (int q = 0; q < D; ++q) o[r * D + q] = obs_feature<TASK, Real>(c, v, r, q, bdim);

@@ -233,7 +233,16 @@ struct EnvView {
     Real* tf;
     int* ti;
     int N;
+    const int* drones;  // arctic: robot index of the k-th drone (robot-index order), else unused
 };
+
+// arctic drone list (het row [1,0,0]) in robot-index order; returns the count
+__host__ __device__ inline int arctic_drones(const mrsim_cfg& c, int* out) {
+    int nd = 0;
+    for (int i = 0; i < c.num_robots; ++i)
+        if (c.het[i][0] == 1.0) out[nd++] = i;
+    return nd;
+}
 
 // ArcticTransportScenario::tile_at (arctic_transport.hpp:47-55): truncating
 // casts, then clamp to the grid.
@@ -580,9 +589,7 @@ __device__ float obs_feature(const mrsim_cfg& c, const EnvView<Real>& v, int r, 
         if (f == 0) return static_cast<float>(arctic_tile_at<Real>(c, v.ti, v.xs[r], v.ys[r]));
         const int g2 = f - 1;
         const int which = g2 / 9, cell = g2 % 9;
-        int d = -1, seen = -1;  // which-th drone in robot-index order
-        for (int i = 0; i < N; ++i)
-            if (c.het[i][0] == 1.0 && ++seen == which) { d = i; break; }
+        const int d = v.drones[which];  // which-th drone in robot-index order
         const int cols = L.arctic_grid_cols, rows = L.arctic_grid_rows;
         const Real hw = Real(c.arena_half_width), hh = Real(c.arena_half_height);
         const Real cw = (hw - (-hw)) / Real(cols);
