@@ -255,6 +255,7 @@ int do_step(mrsim_ctx* ctx, DevState<Real>* s, const int8_t* actions, float* obs
     p.episode_stride = ctx->episode_stride;
     p.smem_bytes_per_group = ctx->smem_group;
     mrsim_host::fill_consts(ctx->cfg, p.k);
+    mrsim_dev::prey_offsets(ctx->cfg, p.prey_off);
     const int smem = ctx->smem_group * (ctx->block / ctx->L);
     cudaError_t e = dispatch_step<Real>(ctx->cfg.task, p, ctx->var, ctx->grid, ctx->block, smem, stream);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "step kernel launch");

@@ -78,6 +78,7 @@ struct StepParams {
     long long episode_stride;
     int smem_bytes_per_group;
     PhysConsts<Real> k;
+    double prey_off[16];  // predator_prey candidate offsets (host-computed with the reference's libm)
 };
 
 // Lexicographic pair index -> (i, j), i < j (barrier.hpp:69-83 order).
@@ -420,7 +421,7 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L)) step_kernel(const __
     BarrierRows<Real, L, MP, MO> rows;
     init_rows(rows, lane, N, p.k.cap);
     const int total_rows_base = rows.P + 4 * N + 4 * N;
-    const EnvView<Real> view{sm.xs, sm.ys, sm.ts, sm.tf, sm.ti, N, sm.drones};
+    const EnvView<Real> view{sm.xs, sm.ys, sm.ts, sm.tf, sm.ti, N, sm.drones, p.prey_off};
     const long long stride = static_cast<long long>(gridDim.x) * gpb;
 
     for (long long e0 = static_cast<long long>(blockIdx.x) * gpb + (gib & ~(G - 1)); e0 < p.B; e0 += stride) {
@@ -745,7 +746,7 @@ __global__ void __launch_bounds__(128) reset_kernel(const __grid_constant__ Rese
     if (p.obs) {
         int drones[MRSIM_MAX_ROBOTS];
         arctic_drones(c, drones);
-        const EnvView<Real> v{xs, ys, ts, tf, ro.ti, N, drones};
+        const EnvView<Real> v{xs, ys, ts, tf, ro.ti, N, drones, nullptr};
         float* o = p.obs + e * N * p.D;
         for (int r = 0; r < N; ++r)
             for (int q = 0; q < p.D; ++q) o[r * p.D + q] = obs_feature<TASK, Real>(c, v, r, q, p.bdim);
@@ -769,7 +770,7 @@ __global__ void __launch_bounds__(128) observe_kernel(const __grid_constant__ mr
     for (int w = 0; w < ni; ++w) ti[w] = s.ti[static_cast<long long>(w) * B + e];
     int drones[MRSIM_MAX_ROBOTS];
     arctic_drones(c, drones);
-    const EnvView<Real> v{xs, ys, ts, tf, ti, N, drones};
+    const EnvView<Real> v{xs, ys, ts, tf, ti, N, drones, nullptr};
     float* o = obs + e * N * D;
     for (int r = 0; r < N; ++r)
         for (int q = 0; q < D; ++q) o[r * D + q] = obs_feature<TASK, Real>(c, v, r, q, bdim);

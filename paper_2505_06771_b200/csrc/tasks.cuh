@@ -20,6 +20,8 @@
 //   warehouse          TI: loaded mask
 #pragma once
 
+#include <cmath>
+
 #include "mrsim_device.cuh"
 
 namespace mrsim_dev {
@@ -234,7 +236,21 @@ struct EnvView {
     int* ti;
     int N;
     const int* drones;  // arctic: robot index of the k-th drone (robot-index order), else unused
+    const double* prey_off;  // predator_prey: 8 candidate offsets (x, y), else unused
 };
+
+// predator_prey: prey_step = agility * max step size (predator_prey.hpp:177-181) and the
+// 8 compass offsets Vec2{cos(ang), sin(ang)} * prey_step, ang = (k-1) pi/4 (predator_prey.hpp:128-133)
+inline void prey_offsets(const mrsim_cfg& c, double* out16) {
+    double robot_step = 0.0;
+    for (int i = 0; i < c.num_robots; ++i) robot_step = robot_step < c.step_sizes[i] ? c.step_sizes[i] : robot_step;
+    const double prey_step = c.layout.pp_prey_agility * robot_step;
+    for (int k = 1; k < 9; ++k) {
+        const double ang = (k - 1) * (3.14159265358979323846 / 4.0);
+        out16[2 * (k - 1)] = std::cos(ang) * prey_step;
+        out16[2 * (k - 1) + 1] = std::sin(ang) * prey_step;
+    }
+}
 
 // arctic drone list (het row [1,0,0]) in robot-index order; returns the count
 __host__ __device__ inline int arctic_drones(const mrsim_cfg& c, int* out) {
@@ -286,19 +302,15 @@ __device__ Real transition_task(const mrsim_cfg& c, EnvView<Real>& v, Rng& rng, 
         for (int i = 0; i < N; ++i) total += dhypot(v.xs[i] - v.tf[2 * i], v.ys[i] - v.tf[2 * i + 1]);
         return Real(c.coef[MRSIM_COEF_DIST]) * total;
     } else if (TASK == MRSIM_TASK_PREDATOR_PREY) {  // predator_prey.hpp:121-143, 183-199
-        double robot_step = 0.0;
-        for (int i = 0; i < N; ++i) robot_step = fmax(robot_step, c.step_sizes[i]);
-        const double prey_step = L.pp_prey_agility * robot_step;
         const Real hw = Real(c.arena_half_width), hh = Real(c.arena_half_height);
         const Real px = v.tf[0], py = v.tf[1];
         Real bx = px, by = py;
         Real best = -Consts<Real>::inf;
         for (int k = 0; k < 9; ++k) {
             Real cx = px, cy = py;
-            if (k > 0) {
-                const double ang = (k - 1) * (3.14159265358979323846 / 4.0);
-                cx = px + Real(__dmul_rn(cos(ang), prey_step));
-                cy = py + Real(__dmul_rn(sin(ang), prey_step));
+            if (k > 0) {  // candidate offsets cos/sin((k-1) pi/4) * prey_step, precomputed on the host
+                cx = px + Real(v.prey_off[2 * (k - 1)]);
+                cy = py + Real(v.prey_off[2 * (k - 1) + 1]);
             }
             if (!(cx >= -hw && cx <= hw && cy >= -hh && cy <= hh)) continue;
             Real nearest = Consts<Real>::inf;
