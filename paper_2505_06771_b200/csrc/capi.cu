@@ -583,8 +583,9 @@ int mrsim_create(const mrsim_cfg* cfg, int device, int64_t num_envs, uint32_t fl
     cudaMemcpy(ctx->d_err, &none, sizeof none, cudaMemcpyHostToDevice);
     cudaMemset(ctx->d_err_serial, 0xff, 8);
     // launch geometry: persistent grid of (SMs x resident blocks)
-    ctx->smem_group = ctx->fp64 ? mrsim_dev::GroupSmem<double>::bytes(ctx->N, ctx->nf, ctx->ni)
-                                : mrsim_dev::GroupSmem<float>::bytes(ctx->N, ctx->nf, ctx->ni);
+    ctx->smem_group =
+        ctx->fp64 ? mrsim_dev::GroupSmem<double>::bytes(ctx->N, ctx->nf, ctx->ni, ctx->var.L, ctx->var.MP, ctx->var.MO)
+                  : mrsim_dev::GroupSmem<float>::bytes(ctx->N, ctx->nf, ctx->ni, ctx->var.L, ctx->var.MP, ctx->var.MO);
     const int smem = ctx->smem_group * (ctx->block / ctx->L);
     int bps = 0;
     e = ctx->fp64 ? dispatch_occ<double>(cfg->task, ctx->var, ctx->block, smem, &bps)

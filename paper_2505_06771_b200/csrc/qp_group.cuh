@@ -130,7 +130,7 @@ __device__ __forceinline__ void qp_drop(const Grp<L>& g, RowSet& rows, const QpW
 // Solve for the groups with `participate` set. (ux, uy): this lane's pair of
 // variables (in: u_nom, out: solution). Returns the QpStatusDev of the group.
 template <class Real, int L, class RowSet>
-__device__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpWs<Real>& ws, int n, bool participate, Real& ux,
+__device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpWs<Real>& ws, int n, bool participate, Real& ux,
                         Real& uy, int total_rows, Real tol) {
     const int lane = g.lane;
     const bool vl = 2 * lane < n;      // this lane's x variable exists

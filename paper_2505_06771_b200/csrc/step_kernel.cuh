@@ -110,18 +110,23 @@ struct LaneCfg {  // pair slots per lane for N <= L robots: ceil(L(L-1)/2 / L)
 template <class Real, int L, int MP, int MO>
 struct BarrierRows {
     static constexpr int MO1 = MO > 0 ? MO : 1;
+    // Row cache in shared memory, field-major [F][L] so lane-owned rows are
+    // conflict-free and any lane can read the owner's row directly:
+    //   pair slot s: fields 3s (gx), 3s+1 (gy), 3s+2 (rhs); walls: 3MP+w;
+    //   obstacle slot t: 3MP+4+3t (gx), +1 (gy), +2 (rhs)
+    static constexpr int kFields = 3 * MP + 4 + 3 * MO;
+    Real* rc;
     int N, P, off_obs, off_box;
     int npair;
     int pi[MP], pj[MP];
-    Real pgx[MP], pgy[MP], ph[MP];
-    Real wl[4];
     Real cap;
     int nob;
     int oslot[MO1];
-    Real ocx[MO1], ocy[MO1], or2[MO1], ogx[MO1], ogy[MO1], oh[MO1];
+    Real ocx[MO1], ocy[MO1], or2[MO1];
     unsigned active;
     bool valid;  // this lane carries a robot
 
+    __device__ __forceinline__ Real& F(int f, int lane) const { return rc[f * L + lane]; }
     __device__ __forceinline__ int dummy_row() const { return off_box; }
 
     // A lane scans its rows in increasing global index, so the reference's
@@ -141,19 +146,24 @@ struct BarrierRows {
         for (int s = 0; s < MP; ++s) {
             const Real uxi = g.shfl(ux, pi[s]), uyi = g.shfl(uy, pi[s]);
             const Real uxj = g.shfl(ux, pj[s]), uyj = g.shfl(uy, pj[s]);
-            if (s < npair && off(s)) consider(pgx[s] * (uxj - uxi) + pgy[s] * (uyj - uyi) - ph[s], lane + s * L, worst, p);
+            if (s < npair && off(s))
+                consider(F(3 * s, lane) * (uxj - uxi) + F(3 * s + 1, lane) * (uyj - uyi) - F(3 * s + 2, lane),
+                         lane + s * L, worst, p);
         }
         if (valid) {
             const int w0 = P + 4 * lane;
-            if (off(MP + 0)) consider(-ux - wl[0], w0, worst, p);
-            if (off(MP + 1)) consider(ux - wl[1], w0 + 1, worst, p);
-            if (off(MP + 2)) consider(-uy - wl[2], w0 + 2, worst, p);
-            if (off(MP + 3)) consider(uy - wl[3], w0 + 3, worst, p);
+            if (off(MP + 0)) consider(-ux - F(3 * MP + 0, lane), w0, worst, p);
+            if (off(MP + 1)) consider(ux - F(3 * MP + 1, lane), w0 + 1, worst, p);
+            if (off(MP + 2)) consider(-uy - F(3 * MP + 2, lane), w0 + 2, worst, p);
+            if (off(MP + 3)) consider(uy - F(3 * MP + 3, lane), w0 + 3, worst, p);
             if (MO > 0) {
 #pragma unroll
-                for (int t = 0; t < MO1; ++t)
+                for (int t = 0; t < MO1; ++t) {
+                    const int f = 3 * MP + 4 + 3 * t;
                     if (t < nob && off(MP + 8 + t))
-                        consider(ogx[t] * ux + ogy[t] * uy - oh[t], off_obs + lane * MRSIM_MAX_SLOTS + oslot[t], worst, p);
+                        consider(F(f, lane) * ux + F(f + 1, lane) * uy - F(f + 2, lane),
+                                 off_obs + lane * MRSIM_MAX_SLOTS + oslot[t], worst, p);
+                }
             }
             // box sides (fold_rows qp.hpp:126-139): only reachable when |u| > cap
             if (dabs(ux) > cap || dabs(uy) > cap) {
@@ -166,69 +176,52 @@ struct BarrierRows {
         }
     }
 
-    // Component of row p on this lane's robot, and the rhs. Collectives are
-    // unconditional (p may differ between the groups of a warp).
+    // Component of row p on this lane's robot, and the rhs, read from the
+    // owner lane's row cache (shared memory broadcast, no collective).
     __device__ __forceinline__ void fetch(const Grp<L>& g, int p, Real& gx, Real& gy, Real& hp) const {
         const int lane = g.lane;
-        int kind, owner;
-        Real cgx = 0, cgy = 0, ch = 0;
-        int cij = 0;
-        if (p < P) {
-            kind = 0;
-            owner = p & (L - 1);
-            const int s = p / L;
+        // obstacle rows: the owner's slot t holding obstacle o; the shuffle runs
+        // unconditionally on every lane (lockstep), its result is used only for obstacle rows
+        int t_obs = 0;
+        if (MO > 0) {
+            const int q = p - off_obs;
+            const int o = q >= 0 ? q % MRSIM_MAX_SLOTS : 0;
+            const int ow = q >= 0 ? (q / MRSIM_MAX_SLOTS) & (L - 1) : 0;
+            int tt = 0;
 #pragma unroll
-            for (int t = 0; t < MP; ++t)
-                if (t == s) {
-                    cgx = pgx[t];
-                    cgy = pgy[t];
-                    ch = ph[t];
-                    cij = pi[t] | (pj[t] << 8);
-                }
-        } else if (p < off_obs) {
-            kind = 1;
-            const int q = p - P, w = q & 3;
-            owner = q >> 2;
-            cgx = (w == 0) ? Real(-1) : ((w == 1) ? Real(1) : Real(0));
-            cgy = (w == 2) ? Real(-1) : ((w == 3) ? Real(1) : Real(0));
-            ch = wl[w];
-            cij = owner;
-        } else if (p < off_box) {
-            kind = 2;
-            const int q = p - off_obs, o = q % MRSIM_MAX_SLOTS;
-            owner = q / MRSIM_MAX_SLOTS;
-            if (MO > 0) {
-#pragma unroll
-                for (int t = 0; t < MO1; ++t)
-                    if (t < nob && oslot[t] == o) {
-                        cgx = ogx[t];
-                        cgy = ogy[t];
-                        ch = oh[t];
-                    }
-            }
-            cij = owner;
-        } else {
-            kind = 3;
-            const int q = p - off_box, b = q & 3;
-            owner = q >> 2;
-            cgx = (b == 0) ? Real(1) : ((b == 1) ? Real(-1) : Real(0));
-            cgy = (b == 2) ? Real(1) : ((b == 3) ? Real(-1) : Real(0));
-            ch = cap;
-            cij = owner;
+            for (int u = 0; u < MO1; ++u)
+                if (u < nob && oslot[u] == o) tt = u;
+            t_obs = g.shfl(tt, ow);
         }
-        const Real bgx = g.shfl(cgx, owner), bgy = g.shfl(cgy, owner);
-        hp = g.shfl(ch, owner);
-        const int bij = g.shfl(cij, owner);
-        if (kind == 0) {
-            const int i = bij & 0xff, j = bij >> 8;
+        if (p < P) {
+            const int owner = p & (L - 1), s = p / L;
+            const Real bgx = F(3 * s, owner), bgy = F(3 * s + 1, owner);
+            hp = F(3 * s + 2, owner);
+            int i = 0, j = 0;
+            pair_of_fast(p, i, j);
             const Real sgn = (lane == j) ? Real(1) : ((lane == i) ? Real(-1) : Real(0));
             gx = sgn * bgx;
             gy = sgn * bgy;
+        } else if (p < off_obs) {
+            const int q = p - P, w = q & 3, owner = q >> 2;
+            hp = F(3 * MP + w, owner);
+            gx = (lane == owner) ? ((w == 0) ? Real(-1) : ((w == 1) ? Real(1) : Real(0))) : Real(0);
+            gy = (lane == owner) ? ((w == 2) ? Real(-1) : ((w == 3) ? Real(1) : Real(0))) : Real(0);
+        } else if (p < off_box) {
+            const int owner = (p - off_obs) / MRSIM_MAX_SLOTS;
+            const int f = 3 * MP + 4 + 3 * t_obs;
+            hp = F(f + 2, owner);
+            gx = (lane == owner) ? F(f, owner) : Real(0);
+            gy = (lane == owner) ? F(f + 1, owner) : Real(0);
         } else {
-            gx = (lane == bij) ? bgx : Real(0);
-            gy = (lane == bij) ? bgy : Real(0);
+            const int q = p - off_box, b = q & 3, owner = q >> 2;
+            hp = cap;
+            gx = (lane == owner) ? ((b == 0) ? Real(1) : ((b == 1) ? Real(-1) : Real(0))) : Real(0);
+            gy = (lane == owner) ? ((b == 2) ? Real(1) : ((b == 3) ? Real(-1) : Real(0))) : Real(0);
         }
     }
+    // (i, j) of pair p (lexicographic), via the owner lane's cached pair table
+    __device__ __forceinline__ void pair_of_fast(int p, int& i, int& j) const { pair_of(p, N, i, j); }
 
     __device__ __forceinline__ void set_active(const Grp<L>& g, int p, bool on) {
         int owner, bit;
@@ -256,7 +249,8 @@ struct BarrierRows {
 };
 
 template <class Real, int L, int MP, int MO>
-__device__ __forceinline__ void init_rows(BarrierRows<Real, L, MP, MO>& rows, int lane, int N, Real cap) {
+__device__ __forceinline__ void init_rows(BarrierRows<Real, L, MP, MO>& rows, Real* rc, int lane, int N, Real cap) {
+    rows.rc = rc;
     rows.N = N;
     rows.P = N * (N - 1) / 2;
     rows.off_obs = rows.P + 4 * N;
@@ -284,7 +278,7 @@ __device__ __forceinline__ void init_rows(BarrierRows<Real, L, MP, MO>& rows, in
 // Returns kQpOptimal/kQpIterLimit (commands set), kQpInfeasible (zeroed), or
 // -1 for coincident projected points (domain_error, barrier.hpp:73-74).
 template <class Real, int L, int MP, int MO>
-__device__ int barrier_filter(const Grp<L>& g, BarrierRows<Real, L, MP, MO>& rows, const QpWs<Real>& ws,
+__device__ __forceinline__ int barrier_filter(const Grp<L>& g, BarrierRows<Real, L, MP, MO>& rows, const QpWs<Real>& ws,
                               const PhysConsts<Real>& k, bool participate, Real prx, Real pry, Real cs, Real sn,
                               Real nv, Real nw, int total_rows, Real& cv, Real& cw) {
     const int lane = g.lane;
@@ -304,18 +298,18 @@ __device__ int barrier_filter(const Grp<L>& g, BarrierRows<Real, L, MP, MO>& row
         if (s < rows.npair && dist2 < Real(1e-18)) coincident = true;
         const Real h = dist2 - k.r_eff2;
         const Real inv = rsqrt(Real(8) * dist2);
-        rows.pgx[s] = Real(2) * dx * inv;
-        rows.pgy[s] = Real(2) * dy * inv;
-        rows.ph[s] = k.gamma * h * h * h * inv;
+        rows.F(3 * s, lane) = Real(2) * dx * inv;
+        rows.F(3 * s + 1, lane) = Real(2) * dy * inv;
+        rows.F(3 * s + 2, lane) = k.gamma * h * h * h * inv;
     }
     // walls (barrier.hpp:85-104)
     {
         const Real h0 = prx - k.wall_xmin, h1 = k.wall_xmax - prx;
         const Real h2 = pry - k.wall_ymin, h3 = k.wall_ymax - pry;
-        rows.wl[0] = k.gamma * h0 * h0 * h0;
-        rows.wl[1] = k.gamma * h1 * h1 * h1;
-        rows.wl[2] = k.gamma * h2 * h2 * h2;
-        rows.wl[3] = k.gamma * h3 * h3 * h3;
+        rows.F(3 * MP + 0, lane) = k.gamma * h0 * h0 * h0;
+        rows.F(3 * MP + 1, lane) = k.gamma * h1 * h1 * h1;
+        rows.F(3 * MP + 2, lane) = k.gamma * h2 * h2 * h2;
+        rows.F(3 * MP + 3, lane) = k.gamma * h3 * h3 * h3;
     }
     // static obstacles (barrier.hpp:106-119)
     if (MO > 0) {
@@ -328,13 +322,15 @@ __device__ int barrier_filter(const Grp<L>& g, BarrierRows<Real, L, MP, MO>& row
                 const Real gh = k.gamma * h * h * h;
                 const bool zero = nrm < Real(1e-14);
                 const Real inv = zero ? Real(0) : Real(1) / nrm;
-                rows.ogx[t] = Real(-2) * dx * inv;
-                rows.ogy[t] = Real(-2) * dy * inv;
-                rows.oh[t] = zero ? gh : gh * inv;
+                const int f = 3 * MP + 4 + 3 * t;
+                rows.F(f, lane) = Real(-2) * dx * inv;
+                rows.F(f + 1, lane) = Real(-2) * dy * inv;
+                rows.F(f + 2, lane) = zero ? gh : gh * inv;
             }
         }
     }
-    const bool bad = g.any(coincident);
+    const bool bad = g.any(coincident);  // (the ballot also orders the row-cache writes before the QP reads)
+    Grp<L>::sync();
     rows.active = 0;
     const int status = qp_solve<Real, L>(g, rows, ws, n, participate && !bad, ux, uy, total_rows, k.tol);
     // map back + uniform scale (barrier.hpp:186-204)
@@ -357,24 +353,26 @@ __device__ int barrier_filter(const Grp<L>& g, BarrierRows<Real, L, MP, MO>& row
 template <class Real>
 struct GroupSmem {
     QpWs<Real> qp;
-    Real *xs, *ys, *ts, *tf;
+    Real *xs, *ys, *ts, *tf, *rc;
     int *ti, *misc, *drones;
-    static __host__ __device__ int bytes(int N, int nf, int ni) {
+    static __host__ __device__ int rc_reals(int L, int MP, int MO) { return (3 * MP + 4 + 3 * MO) * L; }
+    static __host__ __device__ int bytes(int N, int nf, int ni, int L, int MP, int MO) {
         const int n = 2 * N;
-        const int reals = QpWs<Real>::reals(n) + 3 * N + nf;
+        const int reals = QpWs<Real>::reals(n) + 3 * N + nf + rc_reals(L, MP, MO);
         const int ints = QpWs<Real>::ints(n) + ni + 2 + N;
         const int b = reals * static_cast<int>(sizeof(Real)) + ints * 4;
         return (b + 15) & ~15;
     }
-    __device__ void carve(unsigned char* base, int N, int nf) {
+    __device__ void carve(unsigned char* base, int N, int nf, int rcr) {
         const int n = 2 * N;
         Real* r = reinterpret_cast<Real*>(base);
-        int* ib = reinterpret_cast<int*>(r + QpWs<Real>::reals(n) + 3 * N + nf);
+        int* ib = reinterpret_cast<int*>(r + QpWs<Real>::reals(n) + 3 * N + nf + rcr);
         qp.carve(r, ib, n);
         xs = r + QpWs<Real>::reals(n);
         ys = xs + N;
         ts = ys + N;
         tf = ts + N;
+        rc = tf + nf;
         ti = ib + QpWs<Real>::ints(n);
         misc = ti;  // misc words follow the ni task words (set by the kernel)
         drones = nullptr;
@@ -410,7 +408,7 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L)) step_kernel(const __
     const mrsim_cfg& c = p.c;
     const int N = p.N;
     GroupSmem<Real> sm;
-    sm.carve(smem_raw + gib * p.smem_bytes_per_group, N, p.nf);
+    sm.carve(smem_raw + gib * p.smem_bytes_per_group, N, p.nf, GroupSmem<Real>::rc_reals(L, MP, MO));
     int* misc = sm.ti + p.ni;
     sm.drones = misc + 2;
     if (TASK == MRSIM_TASK_ARCTIC_TRANSPORT && lane == 0) arctic_drones(c, sm.drones);
@@ -419,7 +417,7 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L)) step_kernel(const __
     const int ri = vl ? lane : 0;
 
     BarrierRows<Real, L, MP, MO> rows;
-    init_rows(rows, lane, N, p.k.cap);
+    init_rows(rows, sm.rc, lane, N, p.k.cap);
     const int total_rows_base = rows.P + 4 * N + 4 * N;
     const EnvView<Real> view{sm.xs, sm.ys, sm.ts, sm.tf, sm.ti, N, sm.drones, p.prey_off};
     const long long stride = static_cast<long long>(gridDim.x) * gpb;

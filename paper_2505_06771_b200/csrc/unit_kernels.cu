@@ -98,7 +98,8 @@ __global__ void __launch_bounds__(128) barrier_batch_kernel(const __grid_constan
     const int n = 2 * N, P = N * (N - 1) / 2;
     QpWs<Real> ws;
     Real* wr = reinterpret_cast<Real*>(smem_raw + gib * smem_group);
-    ws.carve(wr, reinterpret_cast<int*>(wr + QpWs<Real>::reals(n)), n);
+    ws.carve(wr, nullptr, n);
+    Real* rcache = wr + QpWs<Real>::reals(n);
     const bool vl = lane < N;
     const int ri = vl ? lane : 0;
     const double* ps = poses + t * N * 3;
@@ -110,7 +111,7 @@ __global__ void __launch_bounds__(128) barrier_batch_kernel(const __grid_constan
     int status = kQpOptimal;
     if (c.barrier_enabled) {
         BarrierRows<Real, L, MP, MO> rows;
-        init_rows(rows, lane, N, k.cap);
+        init_rows(rows, rcache, lane, N, k.cap);
         // static obstacles with masks (barrier.hpp:106-119), radius inflated (barrier.hpp:157)
         int obs_rows = 0;
         const double infl = c.projection_distance + c.discrete_margin;
@@ -192,8 +193,10 @@ cudaError_t run_barrier(const mrsim_cfg& c, int count, const double* dp, const d
     const int N = c.num_robots;
     const int block = 128;
     const int gpb = block / L;
-    const int sg = ((mrsim_dev::QpWs<Real>::reals(2 * N) * static_cast<int>(sizeof(Real)) +
-                     mrsim_dev::QpWs<Real>::ints(2 * N) * 4) + 15) & ~15;
+    constexpr int MP = mrsim_dev::LaneCfg<L>::kMaxPair;
+    const int sg = ((mrsim_dev::QpWs<Real>::reals(2 * N) +
+                     mrsim_dev::GroupSmem<Real>::rc_reals(L, MP, MRSIM_MAX_SLOTS)) * static_cast<int>(sizeof(Real)) +
+                    15) & ~15;
     const int grid = (count + gpb - 1) / gpb;
     auto kern = mrsim_dev::barrier_batch_kernel<Real, L>;
     if (sg * gpb > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sg * gpb);
