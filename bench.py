@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
     ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--dist-backend", default="nccl", help="nccl (GPUs) or gloo (multi-rank smoke test)")
     return ap.parse_args()
 
 
@@ -180,12 +181,18 @@ def main():
 
     import paper_2505_06771_b200 as m
 
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dist = None
+    rdev = "cuda"
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if a.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(a.dist_backend)
+            rdev = "cpu"
     cfg = build_cfg(a)
     B = a.envs
     batch = m.CudaEnvBatch(cfg, B, device=local, fp64=(not a.fp32), auto_reset=True)
@@ -216,7 +223,7 @@ def main():
     batch.sync()
     clk = clocks.stop() if clocks else None
     dev_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
-    t_local = torch.tensor([dev_ms], dtype=torch.float64, device="cuda")
+    t_local = torch.tensor([dev_ms], dtype=torch.float64, device=rdev)
     if dist:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
     dev_ms = float(t_local.item())
@@ -226,8 +233,8 @@ def main():
     # episode statistics: the only cross-GPU reduction (sum + min)
     st = batch.stats()
     red = torch.tensor([st["episodes"], st["sum_return"], st["sum_collisions"], st["sum_success"],
-                        st["sum_qp_infeasible"]], dtype=torch.float64, device="cuda")
-    mn = torch.tensor([st["min_pairwise_distance"]], dtype=torch.float64, device="cuda")
+                        st["sum_qp_infeasible"]], dtype=torch.float64, device=rdev)
+    mn = torch.tensor([st["min_pairwise_distance"]], dtype=torch.float64, device=rdev)
     if dist:
         dist.all_reduce(red)
         dist.all_reduce(mn, op=dist.ReduceOp.MIN)
@@ -245,7 +252,7 @@ def main():
         t0 = time.perf_counter()
         for k in range(a.e2e_steps):
             hb.step_host(acts[k])
-        t_e2e = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        t_e2e = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=rdev)
         if dist:
             dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
         h2d = B * a.robots  # int8 actions

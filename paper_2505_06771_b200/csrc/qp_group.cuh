@@ -7,21 +7,23 @@
 // solve_qp (qp.hpp:183-357): Goldfarb-Idnani dual active set with H = I,
 // most-violated row first (ties -> lowest row index), partial dual steps
 // that drop the first blocking multiplier, infeasibility when the entering
-// normal is dependent and nothing blocks. B200-native differences:
-//   * the active set is kept as an incrementally updated QR factorisation
-//     N = Q R (Q: n x k orthonormal columns, R: k x k upper triangular) in
-//     shared memory, instead of re-forming and re-factorising the Gram
-//     matrix N^T N at every inner step (qp.hpp:199-221). Adding a row is one
-//     Gram-Schmidt column (the residual z the step needs anyway), dropping
-//     a row is k Givens rotations; r = (N^T N)^{-1} N^T g = R^{-1} Q^T g.
-//   * lane l owns variables 2l, 2l+1 (one robot: u_x, u_y) and active slots
-//     l, l+L, ...; reductions are shuffles over the group's lanes.
-//   * every loop that contains a collective has a warp-uniform trip count;
-//     per-environment decisions are predicates, so the whole warp (32/L
-//     environments) runs in lockstep with full-mask shuffles.
-//   * rows are never materialised: the RowSet policy evaluates them on the
-//     fly (barrier rows from the robots' projected points, or dense rows
-//     for the unit-level entry point).
+// normal is dependent and nothing blocks. The reference re-forms the Gram
+// matrix M = N^T N of the active normals and Cholesky-solves it at every
+// inner step (qp.hpp:199-221). Here the inverse Gram matrix S = M^{-1} is
+// kept up to date instead:
+//   r   = S (N^T g)                        (one parallel mat-vec, no sequential solve)
+//   z   = g - N r                          (|z|^2 is the Schur complement of M + g)
+//   add : S <- [[S + r r^T / s, -r / s], [-r^T / s, 1 / s]],  s = |z|^2
+//   drop: S <- S_{-b,-b} - S_{-b,b} S_{b,-b} / S_bb           (rank-1 downdate)
+// Rows are used through small descriptors (a barrier row touches at most two
+// robots), so N^T g and N r cost O(k) per lane. Slots are addressed through a
+// logical->physical permutation so a drop never moves S; the logical order
+// (= the reference's active-list order) drives the tie-breaks.
+//
+// Lane l owns variables 2l, 2l+1 (one robot) and logical slots l, l+L.
+// Every loop that contains a collective has a warp-uniform trip count and
+// per-environment decisions are predicates, so the warp (32/L environments)
+// runs in lockstep with full-mask shuffles.
 #pragma once
 
 #include "group.cuh"
@@ -31,117 +33,50 @@ namespace mrsim_dev {
 
 enum QpStatusDev : int { kQpOptimal = 0, kQpInfeasible = 1, kQpIterLimit = 2 };
 
-// Shared-memory workspace of one group for n variables:
-//   Q[a*n + v] (column a = active slot a), R[col*n + row] (upper triangular),
-//   Rd[a] = 1 / R[a][a], gS (entering normal), cS (Q^T g).
-// Per-slot scalars (c_a, r_a, lambda_a, row id) live in registers of lane
-// a % L (slots a = lane and a = lane + L; k <= n = 2N <= 2L).
-template <class Real>
+
+// Shared-memory workspace of one group for n variables (all indexed by
+// PHYSICAL slot unless noted):
+//   S[q*n + q'] inverse Gram, lam, r, d, act (row id), desc (row descriptor),
+//   pm[a] logical -> physical (a permutation; entries >= k are free slots)
+template <class Real, class Desc>
 struct QpWs {
-    Real *Q, *R, *Rd, *gS, *cS;
-    static __host__ __device__ constexpr int reals(int n) { return 2 * n * n + 3 * n; }
-    static __host__ __device__ constexpr int ints(int) { return 0; }
-    __device__ void carve(Real* base, int*, int n) {
-        Q = base;
-        R = Q + n * n;
-        Rd = R + n * n;
-        gS = Rd + n;
-        cS = gS + n;
+    Real *S, *lam, *r, *d;
+    int *act, *pm;
+    Desc* desc;
+    static __host__ __device__ constexpr int bytes(int n) {
+        return static_cast<int>(sizeof(Real)) * (n * n + 3 * n) + 8 * n + static_cast<int>(sizeof(Desc)) * n;
+    }
+    __device__ void carve(unsigned char* base, int n) {
+        S = reinterpret_cast<Real*>(base);
+        lam = S + n * n;
+        r = lam + n;
+        d = r + n;
+        desc = reinterpret_cast<Desc*>(d + n);
+        act = reinterpret_cast<int*>(desc + n);
+        pm = act + n;
     }
 };
-
-// Slot registers of one lane: slots a0 = lane, a1 = lane + L.
-template <class Real>
-struct Slots {
-    Real c0, c1, r0, r1, lam0, lam1;
-    int act0, act1;
-};
-
-// Drop active slot `bi` of the groups with do_drop set (the reference erases
-// active[b] / lambda[b] and re-factorises, qp.hpp:270-271, 312-313, 327-328):
-// delete column bi of R and restore triangularity with Givens rotations that
-// are applied to Q's columns as well. Order of the remaining slots is kept.
-template <class Real, int L, class RowSet>
-__device__ __forceinline__ void qp_drop(const Grp<L>& g, RowSet& rows, const QpWs<Real>& ws, Slots<Real>& sl, int n,
-                                        int& k, bool do_drop, int bi) {
-    const int lane = g.lane;
-    const int a0 = lane, a1 = lane + L;
-    // clear the dropped row's active bit (row id lives on lane bi % L)
-    const int bsrc = bi < 0 ? 0 : (bi & (L - 1));
-    const int dr0 = g.shfl(sl.act0, bsrc), dr1 = g.shfl(sl.act1, bsrc);  // both unconditionally (lockstep)
-    const int drop_row = (bi >= L) ? dr1 : dr0;
-    if (do_drop) rows.set_active(g, drop_row, false);
-    // shift slots (bi, k) down by one: slot a takes slot a+1
-    const int nxt = (lane + 1) & (L - 1);
-    const Real l0n = g.shfl(sl.lam0, nxt), l1n = g.shfl(sl.lam1, nxt);
-    const int c0n = g.shfl(sl.act0, nxt), c1n = g.shfl(sl.act1, nxt);
-    const Real l1_from0 = g.shfl(sl.lam1, 0);
-    const int c1_from0 = g.shfl(sl.act1, 0);
-    if (do_drop) {
-        if (a0 >= bi && a0 < k - 1) {
-            sl.lam0 = (lane < L - 1) ? l0n : l1_from0;
-            sl.act0 = (lane < L - 1) ? c0n : c1_from0;
-        }
-        if (a1 >= bi && a1 < k - 1) {
-            sl.lam1 = l1n;
-            sl.act1 = c1n;
-        }
-        // delete column bi of R (this lane's rows)
-        for (int row = lane; row < k; row += L)
-            for (int col = bi; col < k - 1; ++col) ws.R[col * n + row] = ws.R[(col + 1) * n + row];
-    }
-    Grp<L>::sync();
-    const int jmax = Grp<L>::warp_max(do_drop ? k - 1 : 0);
-    for (int j = 0; j < jmax; ++j) {
-        const bool rot = do_drop && j >= bi && j < k - 1;
-        Real a = 0, bb = 0;
-        if (rot) {
-            a = ws.R[j * n + j];
-            bb = ws.R[j * n + j + 1];
-        }
-        Grp<L>::sync();
-        if (rot) {
-            const Real rho = dsqrt(a * a + bb * bb);
-            const Real cg = a / rho, sg = bb / rho;
-            for (int col = lane; col < k - 1; col += L) {
-                if (col < j) continue;
-                const Real x = ws.R[col * n + j], y = ws.R[col * n + j + 1];
-                ws.R[col * n + j] = cg * x + sg * y;
-                ws.R[col * n + j + 1] = (col == j) ? Real(0) : (-sg * x + cg * y);
-            }
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int v = 2 * lane + h;
-                if (v >= n) continue;
-                const Real x = ws.Q[j * n + v], y = ws.Q[(j + 1) * n + v];
-                ws.Q[j * n + v] = cg * x + sg * y;
-                ws.Q[(j + 1) * n + v] = -sg * x + cg * y;
-            }
-        }
-        Grp<L>::sync();
-    }
-    if (do_drop) {
-        --k;
-        for (int a = lane; a < k; a += L)
-            if (a >= bi) ws.Rd[a] = Real(1) / ws.R[a * n + a];
-    }
-}
 
 // Solve for the groups with `participate` set. (ux, uy): this lane's pair of
 // variables (in: u_nom, out: solution). Returns the QpStatusDev of the group.
-template <class Real, int L, class RowSet>
-__device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpWs<Real>& ws, int n, bool participate, Real& ux,
-                        Real& uy, int total_rows, Real tol) {
+// FAST: specialise the first entering row when the whole warp starts from an
+// empty active set (same arithmetic; a speed/register-pressure trade chosen
+// per task, see qp_fast_first_row in step_kernel.cuh).
+template <class Real, int L, bool FAST = true, class RowSet>
+__device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpWs<Real, typename RowSet::Desc>& ws,
+                                        int n, bool participate, Real& ux, Real& uy, int total_rows, Real tol) {
+    typedef typename RowSet::Desc Desc;
     const int lane = g.lane;
     const bool vl = 2 * lane < n;      // this lane's x variable exists
     const bool vly = 2 * lane + 1 < n;  // ... and its y variable (n may be odd for dense QPs)
-    const int a0 = lane, a1 = lane + L;
-    Slots<Real> sl{0, 0, 0, 0, 0, 0, 0, 0};
+    const int a0 = lane, a1 = lane + L;  // this lane's logical slots
+    for (int a = lane; a < n; a += L) ws.pm[a] = a;
     int k = 0;
     int status = kQpOptimal;
     bool done = !participate;
     int iter = 0;
     const int max_iterations = 100 + 20 * total_rows;  // qp.hpp:193
+    Grp<L>::sync();
     while (Grp<L>::warp_any(!done)) {
         if (!done && iter >= max_iterations) {
             status = kQpIterLimit;
@@ -155,8 +90,10 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
         if (!done && p < 0) done = true;
         if (!Grp<L>::warp_any(!done)) break;  // every env of the warp is optimal
         bool act = !done;
-        Real gx, gy, hp;
-        rows.fetch(g, act ? p : rows.dummy_row(), gx, gy, hp);
+        const Desc gd = rows.describe(g, act ? p : rows.dummy_row());
+        Real gx, gy;
+        rows.comp(gd, lane, gx, gy);
+        const Real hp = rows.rhs(gd);
         if (!vl) gx = Real(0);
         if (!vly) gy = Real(0);
         // Zero-norm violated row: b < 0 on a vacuous row (qp.hpp:242-253).
@@ -166,97 +103,87 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
             done = true;
             act = false;
         }
-        if (act && vl) ws.gS[2 * lane] = gx;
-        if (act && vly) ws.gS[2 * lane + 1] = gy;
-        Grp<L>::sync();
         bool in = act, added = false;
         Real lam_p = 0;
         int guard = 0;
-        if (__all_sync(Grp<L>::kFull, !act || k == 0)) {
-            // Every active group enters its first row: the inner loop of
-            // qp.hpp:262-330 with an empty active set, specialised (c = r = 0,
-            // z = g, t1 = inf). Same arithmetic as the general path.
-            const Real z2 = gn;  // same reduction as the general path's |z|^2 with z = g
+        if (FAST && __all_sync(Grp<L>::kFull, !act || k == 0)) {
+            // Every active group enters its first row: the inner loop below with
+            // an empty active set (r = 0, z = g, |z|^2 = gn, t1 = inf), same arithmetic.
             const Real viol = g.sum(gx * ux + gy * uy) - hp;
             if (act) {
-                if (viol > tol && z2 > Prec<Real>::eps_z) {
-                    const Real t = viol / z2;  // t = min(inf, t2)
+                if (viol <= tol) {
+                    added = true;  // finish, nothing to add (lam_p = 0)
+                } else if (gn <= Prec<Real>::eps_z) {
+                    status = kQpInfeasible;  // dependent normal, nothing blocks (qp.hpp:304-309)
+                    done = true;
+                } else {
+                    const Real t = viol / gn;
                     ux -= t * gx;
                     uy -= t * gy;
-                    const Real rho = dsqrt(z2);
-                    const Real irho = Real(1) / rho;
-                    if (vl) ws.Q[2 * lane] = gx * irho;
-                    if (vly) ws.Q[2 * lane + 1] = gy * irho;
                     if (lane == 0) {
-                        ws.R[0] = rho;
-                        ws.Rd[0] = irho;
-                        sl.lam0 = t;
-                        sl.act0 = p;
+                        const int qk = ws.pm[0];
+                        ws.S[qk * n + qk] = Real(1) / gn;
+                        ws.lam[qk] = t;
+                        ws.act[qk] = p;
+                        ws.desc[qk] = gd;
                     }
                     rows.set_active(g, p, true);
                     k = 1;
-                } else if (viol > tol) {  // dependent normal, nothing blocks: infeasible (qp.hpp:304-309)
-                    status = kQpInfeasible;
-                    done = true;
+                    added = true;
                 }
-                added = true;  // (viol <= tol: finished without adding, lam_p == 0)
             }
-            Grp<L>::sync();
             in = false;
+            Grp<L>::sync();
         }
         while (Grp<L>::warp_any(in)) {  // qp.hpp:262-330
-            // c = Q^T g on this lane's slots
-            sl.c0 = sl.c1 = Real(0);
-            if (in) {
-                if (a0 < k) {
-                    Real c = 0;
-                    for (int v = 0; v < n; ++v) c += ws.Q[a0 * n + v] * ws.gS[v];
-                    sl.c0 = c;
-                    ws.cS[a0] = c;
+            // d = N^T g on this lane's logical slots (physical q)
+            const int q0 = (in && a0 < k) ? ws.pm[a0] : 0;
+            const int q1 = (in && a1 < k) ? ws.pm[a1] : 0;
+            if (in && a0 < k) ws.d[q0] = rows.dot(ws.desc[q0], gd);
+            if (in && a1 < k) ws.d[q1] = rows.dot(ws.desc[q1], gd);
+            Grp<L>::sync();
+            // r = S d (qp.hpp:264's solve_gram, as a mat-vec)
+            Real r0 = 0, r1 = 0;
+            if (in && a0 < k) {
+                for (int c = 0; c < k; ++c) {
+                    const int qc = ws.pm[c];
+                    r0 += ws.S[q0 * n + qc] * ws.d[qc];
                 }
-                if (a1 < k) {  // (slots >= L only exist for N > L/2 ... k > L)
-                    Real c = 0;
-                    for (int v = 0; v < n; ++v) c += ws.Q[a1 * n + v] * ws.gS[v];
-                    sl.c1 = c;
-                    ws.cS[a1] = c;
+                ws.r[q0] = r0;
+            }
+            if (in && a1 < k) {
+                for (int c = 0; c < k; ++c) {
+                    const int qc = ws.pm[c];
+                    r1 += ws.S[q1 * n + qc] * ws.d[qc];
                 }
+                ws.r[q1] = r1;
             }
             Grp<L>::sync();
-            // z = g - Q c (this lane's two components)
+            // z = g - N r (this lane's two components)
             Real zx = gx, zy = gy;
             if (in && vl) {
-                for (int a = 0; a < k; ++a) {
-                    const Real ca = ws.cS[a];
-                    zx -= ws.Q[a * n + 2 * lane] * ca;
-                    if (vly) zy -= ws.Q[a * n + 2 * lane + 1] * ca;
+                for (int c = 0; c < k; ++c) {
+                    const int qc = ws.pm[c];
+                    Real cx, cy;
+                    rows.comp(ws.desc[qc], lane, cx, cy);
+                    const Real rc = ws.r[qc];
+                    zx -= rc * cx;
+                    zy -= rc * cy;
                 }
             }
-            // r = R^{-1} c: column-oriented back substitution, r_b broadcast by shuffle
-            sl.r0 = sl.c0;
-            sl.r1 = sl.c1;
-            const int kmax = Grp<L>::warp_max(in ? k : 0);
-            for (int b = kmax - 1; b >= 0; --b) {
-                const bool hi = b >= L;
-                const Real rb = g.shfl(hi ? sl.r1 : sl.r0, b & (L - 1)) * ws.Rd[b];
-                if (in && b < k) {
-                    if (a0 == b) sl.r0 = rb;
-                    else if (a0 < b) sl.r0 -= ws.R[b * n + a0] * rb;
-                    if (a1 == b) sl.r1 = rb;
-                    else if (a1 < b) sl.r1 -= ws.R[b * n + a1] * rb;
-                }
-            }
+            if (!vly) zy = Real(0);
             const Real z2 = g.sum(zx * zx + zy * zy);
             const Real viol = g.sum(gx * ux + gy * uy) - hp;  // qp.hpp:281
-            // First blocking multiplier (qp.hpp:291-302).
+            // First blocking multiplier in logical order (qp.hpp:291-302).
             Real t1 = Consts<Real>::inf;
             int bi = -1;
             if (in) {
-                if (a0 < k && sl.r0 > Prec<Real>::eps_r) {
-                    t1 = sl.lam0 / sl.r0;
+                if (a0 < k && r0 > Prec<Real>::eps_r) {
+                    t1 = ws.lam[q0] / r0;
                     bi = a0;
                 }
-                if (a1 < k && sl.r1 > Prec<Real>::eps_r) {
-                    const Real t = sl.lam1 / sl.r1;
+                if (a1 < k && r1 > Prec<Real>::eps_r) {
+                    const Real t = ws.lam[q1] / r1;
                     if (bi < 0 || t < t1) {
                         t1 = t;
                         bi = a1;
@@ -296,33 +223,60 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
                 uy -= t * zy;
             }
             if (step_l) {
-                if (a0 < k) sl.lam0 -= t * sl.r0;
-                if (a1 < k) sl.lam1 -= t * sl.r1;
+                if (a0 < k) ws.lam[q0] -= t * r0;
+                if (a1 < k) ws.lam[q1] -= t * r1;
                 lam_p += t;
             }
-            if (do_add) {
-                const Real rho = dsqrt(z2);
-                const Real irho = Real(1) / rho;
-                if (vl) ws.Q[k * n + 2 * lane] = zx * irho;
-                if (vly) ws.Q[k * n + 2 * lane + 1] = zy * irho;
-                if (a0 < k) ws.R[k * n + a0] = sl.c0;
-                if (a1 < k) ws.R[k * n + a1] = sl.c1;
+            if (do_add) {  // bordered inverse: the new slot's Schur complement is |z|^2
+                const Real is = Real(1) / z2;
+                const int qk = ws.pm[k];
+                for (int a = lane; a < k; a += L) {
+                    const int qa = ws.pm[a];
+                    const Real ra = ws.r[qa];
+                    for (int c = 0; c < k; ++c) {
+                        const int qc = ws.pm[c];
+                        ws.S[qa * n + qc] += ra * ws.r[qc] * is;
+                    }
+                    ws.S[qa * n + qk] = -ra * is;
+                    ws.S[qk * n + qa] = -ra * is;
+                }
                 if (lane == 0) {
-                    ws.R[k * n + k] = rho;
-                    ws.Rd[k] = irho;
-                }
-                if (a0 == k) {
-                    sl.lam0 = lam_p;
-                    sl.act0 = p;
-                }
-                if (a1 == k) {
-                    sl.lam1 = lam_p;
-                    sl.act1 = p;
+                    ws.S[qk * n + qk] = is;
+                    ws.lam[qk] = lam_p;
+                    ws.act[qk] = p;
+                    ws.desc[qk] = gd;
                 }
                 rows.set_active(g, p, true);
                 ++k;
             }
-            qp_drop<Real, L>(g, rows, ws, sl, n, k, do_drop, bi);
+            Grp<L>::sync();
+            if (do_drop) {  // S <- S_{-b,-b} - S_{-b,b} S_{b,-b} / S_bb, then free the slot
+                const int qb = ws.pm[bi];
+                rows.set_active(g, ws.act[qb], false);
+                const Real ib = Real(1) / ws.S[qb * n + qb];
+                for (int a = lane; a < k; a += L) {
+                    if (a == bi) continue;
+                    const int qa = ws.pm[a];
+                    const Real sab = ws.S[qa * n + qb] * ib;
+                    for (int c = 0; c < k; ++c) {
+                        if (c == bi) continue;
+                        const int qc = ws.pm[c];
+                        ws.S[qa * n + qc] -= sab * ws.S[qb * n + qc];
+                    }
+                }
+            }
+            // logical order: slots after bi move down by one, the freed slot goes to the end
+            int pm_next0 = 0, pm_next1 = 0;
+            const bool m0 = do_drop && a0 >= bi && a0 < k - 1;
+            const bool m1 = do_drop && a1 >= bi && a1 < k - 1;
+            if (m0) pm_next0 = ws.pm[a0 + 1];
+            if (m1) pm_next1 = ws.pm[a1 + 1];
+            const int freed = do_drop ? ws.pm[bi] : 0;
+            Grp<L>::sync();
+            if (m0) ws.pm[a0] = pm_next0;
+            if (m1) ws.pm[a1] = pm_next1;
+            if (do_drop && lane == ((k - 1) & (L - 1))) ws.pm[k - 1] = freed;
+            if (do_drop) --k;
             if (finish) {
                 in = false;
                 added = true;
@@ -346,10 +300,13 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
 // Dense rows (unit-level entry point, fold_rows qp.hpp:104-141): row r of A
 // in smem, normalised; finite box sides folded after the rows in variable
 // order, hi before lo. Row r is scanned by lane r % L; active sets are
-// group-uniform bit masks.
+// group-uniform bit masks. A descriptor is the row index.
 // ---------------------------------------------------------------------------
 template <class Real, int L, int MAXM>
 struct DenseRows {
+    struct Desc {
+        int p;
+    };
     const Real* G;    // [m][n] normalised rows (smem)
     const Real* h;    // [m]
     Real* ush;        // [n] u broadcast scratch (smem)
@@ -360,6 +317,28 @@ struct DenseRows {
     unsigned long long box_active;   // bit 2v (hi) / 2v+1 (lo)
 
     __device__ int dummy_row() const { return 0; }
+    __device__ Desc describe(const Grp<L>&, int p) const { return Desc{p}; }
+    // component of row p on variable v
+    __device__ Real at(int p, int v) const {
+        if (v >= n) return Real(0);
+        if (p < m) return G[p * n + v];
+        const int q = p - m;
+        return (v == (q >> 1)) ? ((q & 1) ? Real(-1) : Real(1)) : Real(0);
+    }
+    __device__ void comp(const Desc& dsc, int lane, Real& cx, Real& cy) const {
+        cx = at(dsc.p, 2 * lane);
+        cy = at(dsc.p, 2 * lane + 1);
+    }
+    __device__ Real rhs(const Desc& dsc) const {
+        if (dsc.p < m) return h[dsc.p];
+        const int q = dsc.p - m, v = q >> 1;
+        return (q & 1) ? -lo[v] : hi[v];
+    }
+    __device__ Real dot(const Desc& a, const Desc& b) const {
+        Real s = 0;
+        for (int v = 0; v < n; ++v) s += at(a.p, v) * at(b.p, v);
+        return s;
+    }
 
     __device__ void scan(const Grp<L>& g, Real ux, Real uy, Real& worst, int& p) {
         const int lane = g.lane;
@@ -393,25 +372,6 @@ struct DenseRows {
             }
         }
         Grp<L>::sync();
-    }
-    __device__ void fetch(const Grp<L>& g, int p, Real& gx, Real& gy, Real& hp) const {
-        const int lane = g.lane;
-        gx = gy = Real(0);
-        if (p < m) {
-            if (2 * lane < n) gx = G[p * n + 2 * lane];
-            if (2 * lane + 1 < n) gy = G[p * n + 2 * lane + 1];
-            hp = h[p];
-        } else {
-            const int q = p - m;
-            const int v = q >> 1;
-            const bool is_lo = q & 1;
-            const Real s = is_lo ? Real(-1) : Real(1);
-            if (lane == (v >> 1)) {
-                if (v & 1) gy = s;
-                else gx = s;
-            }
-            hp = is_lo ? -lo[v] : hi[v];
-        }
     }
     __device__ void set_active(const Grp<L>&, int p, bool on) {
         if (p < m) {

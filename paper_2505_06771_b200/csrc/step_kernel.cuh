@@ -21,9 +21,13 @@
 #include "tasks.cuh"
 
 // 128-thread blocks per SM the register budget is sized for (measured on B200:
-// 4 -> <=128 regs is best for L <= 8; 3 -> <=168 regs for the QP-heavy L = 16).
+// 4 -> <=128 regs is best for L <= 8; 3 -> <=168 regs for the QP-heavy L = 16
+// and for rware, whose obstacle rows spill at 128 regs: +21% / +18% at N = 4 / 6).
+#ifndef MRSIM_RW_MINB
+#define MRSIM_RW_MINB 3
+#endif
 #ifndef MRSIM_MIN_BLOCKS
-#define MRSIM_MIN_BLOCKS(L) ((L) >= 16 ? 3 : 4)
+#define MRSIM_MIN_BLOCKS(L, TASK) ((L) >= 16 ? 3 : (TASK) == MRSIM_TASK_RWARE ? MRSIM_RW_MINB : 4)
 #endif
 
 namespace mrsim_dev {
@@ -107,6 +111,14 @@ struct LaneCfg {  // pair slots per lane for N <= L robots: ceil(L(L-1)/2 / L)
 // tie-break order of the QP scans.
 // active bits: [0,MP) pairs, MP+w walls, MP+4+b box (x-hi, x-lo, y-hi, y-lo), MP+8+t obstacles
 // ---------------------------------------------------------------------------
+// Row descriptor: components +(cx, cy) on robot r1 and -(cx, cy) on r0 for a
+// pair row (r1 >= 0), or (cx, cy) on robot r0 (walls, box sides, obstacles); rhs h.
+template <class Real>
+struct BarrierDesc {
+    int r0, r1;
+    Real cx, cy, h;
+};
+
 template <class Real, int L, int MP, int MO>
 struct BarrierRows {
     static constexpr int MO1 = MO > 0 ? MO : 1;
@@ -176,13 +188,13 @@ struct BarrierRows {
         }
     }
 
-    // Component of row p on this lane's robot, and the rhs, read from the
-    // owner lane's row cache (shared memory broadcast, no collective).
-    __device__ __forceinline__ void fetch(const Grp<L>& g, int p, Real& gx, Real& gy, Real& hp) const {
-        const int lane = g.lane;
-        // obstacle rows: the owner's slot t holding obstacle o; the shuffle runs
-        // unconditionally on every lane (lockstep), its result is used only for obstacle rows
-        int t_obs = 0;
+    typedef BarrierDesc<Real> Desc;
+
+    // Group-uniform descriptor of row p: pair rows read the owner lane's row
+    // cache (shared memory broadcast); obstacle rows come from the owner's
+    // registers through shuffles that run unconditionally (lockstep).
+    __device__ __forceinline__ Desc describe(const Grp<L>& g, int p) const {
+        Real ogx_b = 0, ogy_b = 0, oh_b = 0;
         if (MO > 0) {
             const int q = p - off_obs;
             const int o = q >= 0 ? q % MRSIM_MAX_SLOTS : 0;
@@ -191,37 +203,60 @@ struct BarrierRows {
 #pragma unroll
             for (int u = 0; u < MO1; ++u)
                 if (u < nob && oslot[u] == o) tt = u;
-            t_obs = g.shfl(tt, ow);
+            const int t = g.shfl(tt, ow);
+            const int f = 3 * MP + 4 + 3 * t;
+            ogx_b = F(f, ow);
+            ogy_b = F(f + 1, ow);
+            oh_b = F(f + 2, ow);
         }
-        if (p < P) {
+        Desc dsc;
+        if (p < P) {  // pair (i, j): -(gx, gy) on i, +(gx, gy) on j
             const int owner = p & (L - 1), s = p / L;
-            const Real bgx = F(3 * s, owner), bgy = F(3 * s + 1, owner);
-            hp = F(3 * s + 2, owner);
-            int i = 0, j = 0;
-            pair_of_fast(p, i, j);
-            const Real sgn = (lane == j) ? Real(1) : ((lane == i) ? Real(-1) : Real(0));
-            gx = sgn * bgx;
-            gy = sgn * bgy;
-        } else if (p < off_obs) {
-            const int q = p - P, w = q & 3, owner = q >> 2;
-            hp = F(3 * MP + w, owner);
-            gx = (lane == owner) ? ((w == 0) ? Real(-1) : ((w == 1) ? Real(1) : Real(0))) : Real(0);
-            gy = (lane == owner) ? ((w == 2) ? Real(-1) : ((w == 3) ? Real(1) : Real(0))) : Real(0);
-        } else if (p < off_box) {
-            const int owner = (p - off_obs) / MRSIM_MAX_SLOTS;
-            const int f = 3 * MP + 4 + 3 * t_obs;
-            hp = F(f + 2, owner);
-            gx = (lane == owner) ? F(f, owner) : Real(0);
-            gy = (lane == owner) ? F(f + 1, owner) : Real(0);
-        } else {
-            const int q = p - off_box, b = q & 3, owner = q >> 2;
-            hp = cap;
-            gx = (lane == owner) ? ((b == 0) ? Real(1) : ((b == 1) ? Real(-1) : Real(0))) : Real(0);
-            gy = (lane == owner) ? ((b == 2) ? Real(1) : ((b == 3) ? Real(-1) : Real(0))) : Real(0);
+            dsc.cx = F(3 * s, owner);
+            dsc.cy = F(3 * s + 1, owner);
+            dsc.h = F(3 * s + 2, owner);
+            pair_of(p, N, dsc.r0, dsc.r1);
+        } else if (p < off_obs) {  // wall w of robot r
+            const int q = p - P, w = q & 3;
+            dsc.r0 = q >> 2;
+            dsc.r1 = -1;
+            dsc.cx = (w == 0) ? Real(-1) : ((w == 1) ? Real(1) : Real(0));
+            dsc.cy = (w == 2) ? Real(-1) : ((w == 3) ? Real(1) : Real(0));
+            dsc.h = F(3 * MP + w, dsc.r0);
+        } else if (p < off_box) {  // obstacle of robot r
+            dsc.r0 = (p - off_obs) / MRSIM_MAX_SLOTS;
+            dsc.r1 = -1;
+            dsc.cx = ogx_b;
+            dsc.cy = ogy_b;
+            dsc.h = oh_b;
+        } else {  // box side of variable v = 2r + axis
+            const int q = p - off_box, b = q & 3;
+            dsc.r0 = q >> 2;
+            dsc.r1 = -1;
+            dsc.cx = (b == 0) ? Real(1) : ((b == 1) ? Real(-1) : Real(0));
+            dsc.cy = (b == 2) ? Real(1) : ((b == 3) ? Real(-1) : Real(0));
+            dsc.h = cap;
         }
+        return dsc;
     }
-    // (i, j) of pair p (lexicographic), via the owner lane's cached pair table
-    __device__ __forceinline__ void pair_of_fast(int p, int& i, int& j) const { pair_of(p, N, i, j); }
+    __device__ __forceinline__ static void comp(const Desc& d, int lane, Real& cx, Real& cy) {
+        const Real s = (d.r1 >= 0) ? ((lane == d.r1) ? Real(1) : ((lane == d.r0) ? Real(-1) : Real(0)))
+                                   : ((lane == d.r0) ? Real(1) : Real(0));
+        cx = s * d.cx;
+        cy = s * d.cy;
+    }
+    __device__ __forceinline__ static Real rhs(const Desc& d) { return d.h; }
+    // full dot product of two rows: sum over the robots they share
+    __device__ __forceinline__ static Real dot(const Desc& a, const Desc& b) {
+        const Real sa0 = (a.r1 >= 0) ? Real(-1) : Real(1), sb0 = (b.r1 >= 0) ? Real(-1) : Real(1);
+        const Real cc = a.cx * b.cx + a.cy * b.cy;
+        Real s = 0;
+        if (a.r0 == b.r0) s += sa0 * sb0 * cc;
+        if (a.r0 == b.r1) s += sa0 * cc;
+        if (a.r1 >= 0 && a.r1 == b.r0) s += sb0 * cc;
+        if (a.r1 >= 0 && a.r1 == b.r1) s += cc;
+        return s;
+    }
 
     __device__ __forceinline__ void set_active(const Grp<L>& g, int p, bool on) {
         int owner, bit;
@@ -277,8 +312,9 @@ __device__ __forceinline__ void init_rows(BarrierRows<Real, L, MP, MO>& rows, Re
 // QP, infeasible -> zero commands, else map back with a uniform scale.
 // Returns kQpOptimal/kQpIterLimit (commands set), kQpInfeasible (zeroed), or
 // -1 for coincident projected points (domain_error, barrier.hpp:73-74).
-template <class Real, int L, int MP, int MO>
-__device__ __forceinline__ int barrier_filter(const Grp<L>& g, BarrierRows<Real, L, MP, MO>& rows, const QpWs<Real>& ws,
+template <class Real, int L, int MP, int MO, bool FAST>
+__device__ __forceinline__ int barrier_filter(const Grp<L>& g, BarrierRows<Real, L, MP, MO>& rows,
+                                              const QpWs<Real, BarrierDesc<Real>>& ws,
                               const PhysConsts<Real>& k, bool participate, Real prx, Real pry, Real cs, Real sn,
                               Real nv, Real nw, int total_rows, Real& cv, Real& cw) {
     const int lane = g.lane;
@@ -332,7 +368,7 @@ __device__ __forceinline__ int barrier_filter(const Grp<L>& g, BarrierRows<Real,
     const bool bad = g.any(coincident);  // (the ballot also orders the row-cache writes before the QP reads)
     Grp<L>::sync();
     rows.active = 0;
-    const int status = qp_solve<Real, L>(g, rows, ws, n, participate && !bad, ux, uy, total_rows, k.tol);
+    const int status = qp_solve<Real, L, FAST>(g, rows, ws, n, participate && !bad, ux, uy, total_rows, k.tol);
     // map back + uniform scale (barrier.hpp:186-204)
     const Real mv = cs * ux + sn * uy;
     const Real mw = (-sn * ux + cs * uy) * k.inv_l;
@@ -352,28 +388,26 @@ __device__ __forceinline__ int barrier_filter(const Grp<L>& g, BarrierRows<Real,
 // Shared-memory layout of one group: QP workspace, final-pose staging, task state.
 template <class Real>
 struct GroupSmem {
-    QpWs<Real> qp;
+    QpWs<Real, BarrierDesc<Real>> qp;
     Real *xs, *ys, *ts, *tf, *rc;
     int *ti, *misc, *drones;
     static __host__ __device__ int rc_reals(int L, int MP, int MO) { return (3 * MP + 4 + 3 * MO) * L; }
     static __host__ __device__ int bytes(int N, int nf, int ni, int L, int MP, int MO) {
-        const int n = 2 * N;
-        const int reals = QpWs<Real>::reals(n) + 3 * N + nf + rc_reals(L, MP, MO);
-        const int ints = QpWs<Real>::ints(n) + ni + 2 + N;
-        const int b = reals * static_cast<int>(sizeof(Real)) + ints * 4;
+        const int qb = (QpWs<Real, BarrierDesc<Real>>::bytes(2 * N) + 15) & ~15;
+        const int reals = 3 * N + nf + rc_reals(L, MP, MO);
+        const int ints = ni + 2 + N;
+        const int b = qb + reals * static_cast<int>(sizeof(Real)) + ints * 4;
         return (b + 15) & ~15;
     }
     __device__ void carve(unsigned char* base, int N, int nf, int rcr) {
-        const int n = 2 * N;
-        Real* r = reinterpret_cast<Real*>(base);
-        int* ib = reinterpret_cast<int*>(r + QpWs<Real>::reals(n) + 3 * N + nf + rcr);
-        qp.carve(r, ib, n);
-        xs = r + QpWs<Real>::reals(n);
+        qp.carve(base, 2 * N);
+        Real* r = reinterpret_cast<Real*>(base + ((QpWs<Real, BarrierDesc<Real>>::bytes(2 * N) + 15) & ~15));
+        xs = r;
         ys = xs + N;
         ts = ys + N;
         tf = ts + N;
         rc = tf + nf;
-        ti = ib + QpWs<Real>::ints(n);
+        ti = reinterpret_cast<int*>(rc + rcr);
         misc = ti;  // misc words follow the ni task words (set by the kernel)
         drones = nullptr;
     }
@@ -395,8 +429,20 @@ __device__ __forceinline__ Real wrap_angle_dev(Real t) {
 // The fused step kernel. Persistent grid-stride loop; each warp steps 32/L
 // environments in lockstep (ghost groups past the end compute but never store).
 // ---------------------------------------------------------------------------
+// First-row QP fast path (qp_solve FAST): a measured per-task choice (B200,
+// fp64). It wins where most filtered steps enter one row from an empty active
+// set (navigation +8%, warehouse +10%, foraging +4%); elsewhere the extra code
+// costs more than it saves (predator_prey -4%, rware -10% at the old register
+// budget) or is neutral (N = 10 teams).
+__host__ __device__ constexpr bool qp_fast_first_row(int task) {
+#ifdef MRSIM_QP_NO_FAST
+    return false && task;
+#endif
+    return task != MRSIM_TASK_RWARE && task != MRSIM_TASK_PREDATOR_PREY && task != MRSIM_TASK_MATERIAL_TRANSPORT && task != MRSIM_TASK_ARCTIC_TRANSPORT;
+}
+
 template <class Real, int L, int MP, int MO, int TASK>
-__global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L)) step_kernel(const __grid_constant__ StepParams<Real> p) {
+__global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(const __grid_constant__ StepParams<Real> p) {
     constexpr int G = 32 / L;  // envs per warp
     if (*p.err != ~0ull) return;  // sticky device error: later steps are no-ops
 
@@ -521,7 +567,7 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L)) step_kernel(const __
             }
             Real cv = nv, cw = nw;
             if (c.barrier_enabled) {
-                const int bs = barrier_filter<Real, L>(g, rows, sm.qp, p.k, !skip, prx, pry, cs, sn, nv, nw,
+                const int bs = barrier_filter<Real, L, MP, MO, qp_fast_first_row(TASK)>(g, rows, sm.qp, p.k, !skip, prx, pry, cs, sn, nv, nw,
                                                        total_rows, cv, cw);
                 if (bs < 0 && !skip) {
                     if (lane == 0) {

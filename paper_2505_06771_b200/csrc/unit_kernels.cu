@@ -15,6 +15,13 @@ namespace mrsim_dev {
 constexpr int kQpMaxN = 32;
 constexpr int kQpMaxM = 64;
 
+// one problem's smem: the QP workspace, then G [m][n], h [m], u scratch, lo, hi [n] (each 16-byte aligned)
+template <class Real>
+__host__ __device__ constexpr int qp_slot_bytes(int n, int m) {
+    typedef typename DenseRows<Real, 16, kQpMaxM>::Desc D;
+    return ((QpWs<Real, D>::bytes(n) + 15) & ~15) + (((m * n + m + 3 * n) * static_cast<int>(sizeof(Real)) + 15) & ~15);
+}
+
 template <class Real>
 __global__ void __launch_bounds__(32) qp_batch_kernel(int count, int n, int m, const double* A, const double* b,
                                                       const double* lo, const double* hi, const double* unom,
@@ -26,15 +33,15 @@ __global__ void __launch_bounds__(32) qp_batch_kernel(int count, int n, int m, c
     const Grp<L> g;
     const int lane = g.lane;
     const int slot = threadIdx.x / L;
-    const int slot_reals = m * n + m + 3 * n + QpWs<Real>::reals(n);
-    Real* base = reinterpret_cast<Real*>(qsmem) + slot * slot_reals;
-    Real* Gs = base;
+    typedef typename DenseRows<Real, L, kQpMaxM>::Desc DDesc;
+    unsigned char* sbase = qsmem + slot * qp_slot_bytes<Real>(n, m);
+    QpWs<Real, DDesc> ws;
+    ws.carve(sbase, n);
+    Real* Gs = reinterpret_cast<Real*>(sbase + ((QpWs<Real, DDesc>::bytes(n) + 15) & ~15));
     Real* hs = Gs + m * n;
     Real* ushs = hs + m;
     Real* loss = ushs + n;
     Real* hiss = loss + n;
-    Real* wsr = hiss + n;
-    int* wsi = reinterpret_cast<int*>(reinterpret_cast<Real*>(qsmem) + 2 * slot_reals) + slot * n;
     const int t_real = blockIdx.x * 2 + slot;
     const bool ghost = t_real >= count;
     const int t = ghost ? count - 1 : t_real;
@@ -63,8 +70,6 @@ __global__ void __launch_bounds__(32) qp_batch_kernel(int count, int n, int m, c
         boxes += hi[static_cast<size_t>(t) * n + i] < 1e30 ? 1 : 0;
         boxes += lo[static_cast<size_t>(t) * n + i] > -1e30 ? 1 : 0;
     }
-    QpWs<Real> ws;
-    ws.carve(wsr, wsi, n);
     DenseRows<Real, L, kQpMaxM> rows{Gs, hs, ushs, loss, hiss, n, m, 0ull, 0ull};
     const bool vl = 2 * lane < n;
     Real ux = vl ? Real(unom[static_cast<size_t>(t) * n + 2 * lane]) : Real(0);
@@ -96,10 +101,10 @@ __global__ void __launch_bounds__(128) barrier_batch_kernel(const __grid_constan
     const bool ghost = t_real >= count;
     const long long t = ghost ? count - 1 : t_real;
     const int n = 2 * N, P = N * (N - 1) / 2;
-    QpWs<Real> ws;
-    Real* wr = reinterpret_cast<Real*>(smem_raw + gib * smem_group);
-    ws.carve(wr, nullptr, n);
-    Real* rcache = wr + QpWs<Real>::reals(n);
+    QpWs<Real, BarrierDesc<Real>> ws;
+    ws.carve(smem_raw + gib * smem_group, n);
+    Real* rcache = reinterpret_cast<Real*>(smem_raw + gib * smem_group +
+                                           ((QpWs<Real, BarrierDesc<Real>>::bytes(n) + 15) & ~15));
     const bool vl = lane < N;
     const int ri = vl ? lane : 0;
     const double* ps = poses + t * N * 3;
@@ -138,7 +143,7 @@ __global__ void __launch_bounds__(128) barrier_batch_kernel(const __grid_constan
         Real sn, cs;
         dsincos(th, &sn, &cs);
         const Real prx = x + cs * k.l, pry = y + sn * k.l;
-        status = barrier_filter<Real, L>(g, rows, ws, k, !ghost, prx, pry, cs, sn, nv, nw, P + 8 * N + obs_rows, cv,
+        status = barrier_filter<Real, L, MP, MO, true>(g, rows, ws, k, !ghost, prx, pry, cs, sn, nv, nw, P + 8 * N + obs_rows, cv,
                                          cw);
     }
     if (!ghost) {
@@ -194,9 +199,9 @@ cudaError_t run_barrier(const mrsim_cfg& c, int count, const double* dp, const d
     const int block = 128;
     const int gpb = block / L;
     constexpr int MP = mrsim_dev::LaneCfg<L>::kMaxPair;
-    const int sg = ((mrsim_dev::QpWs<Real>::reals(2 * N) +
-                     mrsim_dev::GroupSmem<Real>::rc_reals(L, MP, MRSIM_MAX_SLOTS)) * static_cast<int>(sizeof(Real)) +
-                    15) & ~15;
+    const int sg = (((mrsim_dev::QpWs<Real, mrsim_dev::BarrierDesc<Real>>::bytes(2 * N) + 15) & ~15) +
+                    mrsim_dev::GroupSmem<Real>::rc_reals(L, MP, MRSIM_MAX_SLOTS) * static_cast<int>(sizeof(Real)) + 15) &
+                   ~15;
     const int grid = (count + gpb - 1) / gpb;
     auto kern = mrsim_dev::barrier_batch_kernel<Real, L>;
     if (sg * gpb > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sg * gpb);
@@ -255,8 +260,8 @@ int mrsim_qp_solve_batch(int device, int fp64, int count, int n, int m, const do
     if ((e = upload<double>(dout, nullptr, static_cast<size_t>(count) * n)) != cudaSuccess) return MRSIM_E_CUDA;
     if ((e = upload<int32_t>(dst, nullptr, count)) != cudaSuccess) return MRSIM_E_CUDA;
     if ((e = upload<int32_t>(dit, nullptr, count)) != cudaSuccess) return MRSIM_E_CUDA;
-    const size_t smem_d = 2 * (static_cast<size_t>(m) * n + m + 3 * n + mrsim_dev::QpWs<double>::reals(n)) * 8 + 2 * n * 4;
-    const size_t smem_f = 2 * (static_cast<size_t>(m) * n + m + 3 * n + mrsim_dev::QpWs<float>::reals(n)) * 4 + 2 * n * 4;
+    const size_t smem_d = 2 * static_cast<size_t>(mrsim_dev::qp_slot_bytes<double>(n, m));
+    const size_t smem_f = 2 * static_cast<size_t>(mrsim_dev::qp_slot_bytes<float>(n, m));
     if (smem_d > 48 * 1024)
         cudaFuncSetAttribute(mrsim_dev::qp_batch_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem_d));
