@@ -51,28 +51,36 @@ struct Grp {
     __device__ __forceinline__ static int warp_max(int v) { return __reduce_max_sync(kFull, v); }
     // argmax with ties to the lowest index (first-maximal `v > worst` scans, qp.hpp:228-238);
     // idx < 0 = none
+    // idx < 0 (none) travels as kNone so it loses every tie; callers pass v =
+    // the scan threshold (argmax) / +inf (argmin) with it, which any real
+    // candidate beats strictly.
+    static constexpr int kNone = 0x7fffffff;
     template <class T>
     __device__ __forceinline__ void argmax(T& v, int& idx) const {
+        idx = idx < 0 ? kNone : idx;
 #pragma unroll
         for (int o = L / 2; o > 0; o >>= 1) {
             const T ov = __shfl_xor_sync(kFull, v, o, L);
             const int oi = __shfl_xor_sync(kFull, idx, o, L);
-            const bool take = (oi >= 0) && (idx < 0 || ov > v || (ov == v && oi < idx));
+            const bool take = ov > v || (ov == v && oi < idx);
             v = take ? ov : v;
             idx = take ? oi : idx;
         }
+        idx = idx == kNone ? -1 : idx;
     }
     // argmin with ties to the lowest index (`t < t1`, qp.hpp:294-302)
     template <class T>
     __device__ __forceinline__ void argmin(T& v, int& idx) const {
+        idx = idx < 0 ? kNone : idx;
 #pragma unroll
         for (int o = L / 2; o > 0; o >>= 1) {
             const T ov = __shfl_xor_sync(kFull, v, o, L);
             const int oi = __shfl_xor_sync(kFull, idx, o, L);
-            const bool take = (oi >= 0) && (idx < 0 || ov < v || (ov == v && oi < idx));
+            const bool take = ov < v || (ov == v && oi < idx);
             v = take ? ov : v;
             idx = take ? oi : idx;
         }
+        idx = idx == kNone ? -1 : idx;
     }
 };
 

@@ -72,6 +72,7 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
     const int a0 = lane, a1 = lane + L;  // this lane's logical slots
     for (int a = lane; a < n; a += L) ws.pm[a] = a;
     int k = 0;
+    unsigned tm = 0;  // physical slots whose row touches this lane's variables (n <= 32)
     int status = kQpOptimal;
     bool done = !participate;
     int iter = 0;
@@ -120,8 +121,9 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
                     const Real t = viol / gn;
                     ux -= t * gx;
                     uy -= t * gy;
+                    const int qk = ws.pm[0];
+                    if (rows.touches(gd, lane)) tm |= 1u << qk;
                     if (lane == 0) {
-                        const int qk = ws.pm[0];
                         ws.S[qk * n + qk] = Real(1) / gn;
                         ws.lam[qk] = t;
                         ws.act[qk] = p;
@@ -162,8 +164,8 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
             // z = g - N r (this lane's two components)
             Real zx = gx, zy = gy;
             if (in && vl) {
-                for (int c = 0; c < k; ++c) {
-                    const int qc = ws.pm[c];
+                for (unsigned m = tm; m; m &= m - 1) {  // only the active rows touching this lane's variables
+                    const int qc = __ffs(m) - 1;
                     Real cx, cy;
                     rows.comp(ws.desc[qc], lane, cx, cy);
                     const Real rc = ws.r[qc];
@@ -240,6 +242,7 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
                     ws.S[qa * n + qk] = -ra * is;
                     ws.S[qk * n + qa] = -ra * is;
                 }
+                if (rows.touches(gd, lane)) tm |= 1u << qk;
                 if (lane == 0) {
                     ws.S[qk * n + qk] = is;
                     ws.lam[qk] = lam_p;
@@ -252,6 +255,7 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
             Grp<L>::sync();
             if (do_drop) {  // S <- S_{-b,-b} - S_{-b,b} S_{b,-b} / S_bb, then free the slot
                 const int qb = ws.pm[bi];
+                tm &= ~(1u << qb);
                 rows.set_active(g, ws.act[qb], false);
                 const Real ib = Real(1) / ws.S[qb * n + qb];
                 for (int a = lane; a < k; a += L) {
@@ -329,6 +333,7 @@ struct DenseRows {
         cx = at(dsc.p, 2 * lane);
         cy = at(dsc.p, 2 * lane + 1);
     }
+    __device__ static bool touches(const Desc&, int) { return true; }
     __device__ Real rhs(const Desc& dsc) const {
         if (dsc.p < m) return h[dsc.p];
         const int q = dsc.p - m, v = q >> 1;

@@ -245,6 +245,7 @@ struct BarrierRows {
         cx = s * d.cx;
         cy = s * d.cy;
     }
+    __device__ __forceinline__ static bool touches(const Desc& d, int lane) { return lane == d.r0 || lane == d.r1; }
     __device__ __forceinline__ static Real rhs(const Desc& d) { return d.h; }
     // full dot product of two rows: sum over the robots they share
     __device__ __forceinline__ static Real dot(const Desc& a, const Desc& b) {
