@@ -34,17 +34,18 @@ namespace mrsim_dev {
 enum QpStatusDev : int { kQpOptimal = 0, kQpInfeasible = 1, kQpIterLimit = 2 };
 
 
-// Shared-memory workspace of one group for n variables (all indexed by
-// PHYSICAL slot unless noted):
-//   S[q*n + q'] inverse Gram, lam, r, d, act (row id), desc (row descriptor),
-//   pm[a] logical -> physical (a permutation; entries >= k are free slots)
+// Shared-memory workspace of one group for n variables, indexed by PHYSICAL
+// slot: S[q*n + q'] inverse Gram, lam, r, d, act (row id), desc (row descriptor).
+// Physical slot q is owned by lane q % L (q < 2L); the owner keeps the slot's
+// logical position (= the reference's active-list order,
+// which drives the tie-breaks) in registers, so a drop never moves data.
 template <class Real, class Desc>
 struct QpWs {
     Real *S, *lam, *r, *d;
-    int *act, *pm;
     Desc* desc;
+    int* act;
     static __host__ __device__ constexpr int bytes(int n) {
-        return static_cast<int>(sizeof(Real)) * (n * n + 3 * n) + 8 * n + static_cast<int>(sizeof(Desc)) * n;
+        return static_cast<int>(sizeof(Real)) * (n * n + 3 * n) + static_cast<int>(sizeof(Desc)) * n + 4 * n;
     }
     __device__ void carve(unsigned char* base, int n) {
         S = reinterpret_cast<Real*>(base);
@@ -53,7 +54,6 @@ struct QpWs {
         d = r + n;
         desc = reinterpret_cast<Desc*>(d + n);
         act = reinterpret_cast<int*>(desc + n);
-        pm = act + n;
     }
 };
 
@@ -69,15 +69,15 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
     const int lane = g.lane;
     const bool vl = 2 * lane < n;      // this lane's x variable exists
     const bool vly = 2 * lane + 1 < n;  // ... and its y variable (n may be odd for dense QPs)
-    const int a0 = lane, a1 = lane + L;  // this lane's logical slots
-    for (int a = lane; a < n; a += L) ws.pm[a] = a;
+    const int q0 = lane, q1 = lane + L;  // this lane's physical slots (n <= 2L)
+    int lp0 = -1, lp1 = -1;              // their logical positions, -1 = free
+    unsigned amask = 0;                  // active physical slots (group-uniform; n <= 32)
+    unsigned tm = 0;                     // active slots whose row touches this lane's variables
     int k = 0;
-    unsigned tm = 0;  // physical slots whose row touches this lane's variables (n <= 32)
     int status = kQpOptimal;
     bool done = !participate;
     int iter = 0;
     const int max_iterations = 100 + 20 * total_rows;  // qp.hpp:193
-    Grp<L>::sync();
     while (Grp<L>::warp_any(!done)) {
         if (!done && iter >= max_iterations) {
             status = kQpIterLimit;
@@ -97,6 +97,7 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
         const Real hp = rows.rhs(gd);
         if (!vl) gx = Real(0);
         if (!vly) gy = Real(0);
+        const bool touch = rows.touches(gd, lane);
         // Zero-norm violated row: b < 0 on a vacuous row (qp.hpp:242-253).
         const Real gn = g.sum(gx * gx + gy * gy);
         if (act && gn < Prec<Real>::eps_row) {
@@ -121,14 +122,15 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
                     const Real t = viol / gn;
                     ux -= t * gx;
                     uy -= t * gy;
-                    const int qk = ws.pm[0];
-                    if (rows.touches(gd, lane)) tm |= 1u << qk;
-                    if (lane == 0) {
-                        ws.S[qk * n + qk] = Real(1) / gn;
-                        ws.lam[qk] = t;
-                        ws.act[qk] = p;
-                        ws.desc[qk] = gd;
+                    if (lane == 0) {  // physical slot 0
+                        ws.S[0] = Real(1) / gn;
+                        ws.act[0] = p;
+                        ws.desc[0] = gd;
+                        ws.lam[0] = t;
+                        lp0 = 0;
                     }
+                    if (touch) tm = 1u;
+                    amask = 1u;
                     rows.set_active(g, p, true);
                     k = 1;
                     added = true;
@@ -138,37 +140,36 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
             Grp<L>::sync();
         }
         while (Grp<L>::warp_any(in)) {  // qp.hpp:262-330
-            // d = N^T g on this lane's logical slots (physical q)
-            const int q0 = (in && a0 < k) ? ws.pm[a0] : 0;
-            const int q1 = (in && a1 < k) ? ws.pm[a1] : 0;
-            if (in && a0 < k) ws.d[q0] = rows.dot(ws.desc[q0], gd);
-            if (in && a1 < k) ws.d[q1] = rows.dot(ws.desc[q1], gd);
+            const bool s0 = in && lp0 >= 0, s1 = in && lp1 >= 0;  // own active slots
+            // d = N^T g
+            if (s0) ws.d[q0] = rows.dot(ws.desc[q0], gd);
+            if (s1) ws.d[q1] = rows.dot(ws.desc[q1], gd);
             Grp<L>::sync();
             // r = S d (qp.hpp:264's solve_gram, as a mat-vec)
             Real r0 = 0, r1 = 0;
-            if (in && a0 < k) {
-                for (int c = 0; c < k; ++c) {
-                    const int qc = ws.pm[c];
-                    r0 += ws.S[q0 * n + qc] * ws.d[qc];
+            if (s0) {
+                for (unsigned m = amask; m; m &= m - 1) {
+                    const int c = __ffs(m) - 1;
+                    r0 += ws.S[q0 * n + c] * ws.d[c];
                 }
                 ws.r[q0] = r0;
             }
-            if (in && a1 < k) {
-                for (int c = 0; c < k; ++c) {
-                    const int qc = ws.pm[c];
-                    r1 += ws.S[q1 * n + qc] * ws.d[qc];
+            if (s1) {
+                for (unsigned m = amask; m; m &= m - 1) {
+                    const int c = __ffs(m) - 1;
+                    r1 += ws.S[q1 * n + c] * ws.d[c];
                 }
                 ws.r[q1] = r1;
             }
             Grp<L>::sync();
-            // z = g - N r (this lane's two components)
+            // z = g - N r (this lane's two components; only the rows touching them)
             Real zx = gx, zy = gy;
             if (in && vl) {
-                for (unsigned m = tm; m; m &= m - 1) {  // only the active rows touching this lane's variables
-                    const int qc = __ffs(m) - 1;
+                for (unsigned m = tm; m; m &= m - 1) {
+                    const int c = __ffs(m) - 1;
                     Real cx, cy;
-                    rows.comp(ws.desc[qc], lane, cx, cy);
-                    const Real rc = ws.r[qc];
+                    rows.comp(ws.desc[c], lane, cx, cy);
+                    const Real rc = ws.r[c];
                     zx -= rc * cx;
                     zy -= rc * cy;
                 }
@@ -176,24 +177,26 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
             if (!vly) zy = Real(0);
             const Real z2 = g.sum(zx * zx + zy * zy);
             const Real viol = g.sum(gx * ux + gy * uy) - hp;  // qp.hpp:281
-            // First blocking multiplier in logical order (qp.hpp:291-302).
+            // First blocking multiplier in logical order (qp.hpp:291-302):
+            // key = logical position * 64 + physical slot.
             Real t1 = Consts<Real>::inf;
-            int bi = -1;
-            if (in) {
-                if (a0 < k && r0 > Prec<Real>::eps_r) {
-                    t1 = ws.lam[q0] / r0;
-                    bi = a0;
-                }
-                if (a1 < k && r1 > Prec<Real>::eps_r) {
-                    const Real t = ws.lam[q1] / r1;
-                    if (bi < 0 || t < t1) {
-                        t1 = t;
-                        bi = a1;
-                    }
+            int bk = -1;
+            if (s0 && r0 > Prec<Real>::eps_r) {
+                t1 = ws.lam[q0] / r0;
+                bk = lp0 * 64 + q0;
+            }
+            if (s1 && r1 > Prec<Real>::eps_r) {
+                const Real t = ws.lam[q1] / r1;
+                const int key = lp1 * 64 + q1;
+                if (bk < 0 || t < t1 || (t == t1 && key < bk)) {
+                    t1 = t;
+                    bk = key;
                 }
             }
-            g.argmin(t1, bi);
-            if (bi < 0) t1 = Consts<Real>::inf;
+            g.argmin(t1, bk);
+            const int bi = bk < 0 ? -1 : (bk >> 6);  // logical position of the blocking slot
+            const int qb = bk < 0 ? 0 : (bk & 63);   // ... and its physical slot
+            if (bk < 0) t1 = Consts<Real>::inf;
             bool finish = false, do_add = false, do_drop = false, infeas = false, step_u = false, step_l = false;
             Real t = 0;
             if (in) {
@@ -225,62 +228,70 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
                 uy -= t * zy;
             }
             if (step_l) {
-                if (a0 < k) ws.lam[q0] -= t * r0;
-                if (a1 < k) ws.lam[q1] -= t * r1;
+                if (s0) ws.lam[q0] -= t * r0;
+                if (s1) ws.lam[q1] -= t * r1;
                 lam_p += t;
             }
             if (do_add) {  // bordered inverse: the new slot's Schur complement is |z|^2
                 const Real is = Real(1) / z2;
-                const int qk = ws.pm[k];
-                for (int a = lane; a < k; a += L) {
-                    const int qa = ws.pm[a];
-                    const Real ra = ws.r[qa];
-                    for (int c = 0; c < k; ++c) {
-                        const int qc = ws.pm[c];
-                        ws.S[qa * n + qc] += ra * ws.r[qc] * is;
+                const int qk = __ffs(~amask) - 1;  // lowest free physical slot
+                if (s0) {
+                    const Real ra = r0 * is;
+                    for (unsigned m = amask; m; m &= m - 1) {
+                        const int c = __ffs(m) - 1;
+                        ws.S[q0 * n + c] += ra * ws.r[c];
                     }
-                    ws.S[qa * n + qk] = -ra * is;
-                    ws.S[qk * n + qa] = -ra * is;
+                    ws.S[q0 * n + qk] = -ra;
+                    ws.S[qk * n + q0] = -ra;
                 }
-                if (rows.touches(gd, lane)) tm |= 1u << qk;
-                if (lane == 0) {
+                if (s1) {
+                    const Real ra = r1 * is;
+                    for (unsigned m = amask; m; m &= m - 1) {
+                        const int c = __ffs(m) - 1;
+                        ws.S[q1 * n + c] += ra * ws.r[c];
+                    }
+                    ws.S[q1 * n + qk] = -ra;
+                    ws.S[qk * n + q1] = -ra;
+                }
+                if (lane == (qk & (L - 1))) {
                     ws.S[qk * n + qk] = is;
-                    ws.lam[qk] = lam_p;
                     ws.act[qk] = p;
                     ws.desc[qk] = gd;
+                    ws.lam[qk] = lam_p;
+                    if (qk < L) lp0 = k;
+                    else lp1 = k;
                 }
+                if (touch) tm |= 1u << qk;
+                amask |= 1u << qk;
                 rows.set_active(g, p, true);
                 ++k;
             }
-            Grp<L>::sync();
-            if (do_drop) {  // S <- S_{-b,-b} - S_{-b,b} S_{b,-b} / S_bb, then free the slot
-                const int qb = ws.pm[bi];
-                tm &= ~(1u << qb);
+            if (do_drop) {  // S <- S_{-b,-b} - S_{-b,b} S_{b,-b} / S_bb; later slots move up one logical place
                 rows.set_active(g, ws.act[qb], false);
+                const unsigned rest = amask & ~(1u << qb);
                 const Real ib = Real(1) / ws.S[qb * n + qb];
-                for (int a = lane; a < k; a += L) {
-                    if (a == bi) continue;
-                    const int qa = ws.pm[a];
-                    const Real sab = ws.S[qa * n + qb] * ib;
-                    for (int c = 0; c < k; ++c) {
-                        if (c == bi) continue;
-                        const int qc = ws.pm[c];
-                        ws.S[qa * n + qc] -= sab * ws.S[qb * n + qc];
+                if (s0 && q0 != qb) {
+                    const Real sab = ws.S[q0 * n + qb] * ib;
+                    for (unsigned m = rest; m; m &= m - 1) {
+                        const int c = __ffs(m) - 1;
+                        ws.S[q0 * n + c] -= sab * ws.S[qb * n + c];
                     }
                 }
+                if (s1 && q1 != qb) {
+                    const Real sab = ws.S[q1 * n + qb] * ib;
+                    for (unsigned m = rest; m; m &= m - 1) {
+                        const int c = __ffs(m) - 1;
+                        ws.S[q1 * n + c] -= sab * ws.S[qb * n + c];
+                    }
+                }
+                if (lp0 > bi) --lp0;
+                if (lp1 > bi) --lp1;
+                if (q0 == qb) lp0 = -1;
+                if (q1 == qb) lp1 = -1;
+                tm &= ~(1u << qb);
+                amask = rest;
+                --k;
             }
-            // logical order: slots after bi move down by one, the freed slot goes to the end
-            int pm_next0 = 0, pm_next1 = 0;
-            const bool m0 = do_drop && a0 >= bi && a0 < k - 1;
-            const bool m1 = do_drop && a1 >= bi && a1 < k - 1;
-            if (m0) pm_next0 = ws.pm[a0 + 1];
-            if (m1) pm_next1 = ws.pm[a1 + 1];
-            const int freed = do_drop ? ws.pm[bi] : 0;
-            Grp<L>::sync();
-            if (m0) ws.pm[a0] = pm_next0;
-            if (m1) ws.pm[a1] = pm_next1;
-            if (do_drop && lane == ((k - 1) & (L - 1))) ws.pm[k - 1] = freed;
-            if (do_drop) --k;
             if (finish) {
                 in = false;
                 added = true;

@@ -125,8 +125,10 @@ struct BarrierRows {
     // Row cache in shared memory, field-major [F][L] so lane-owned rows are
     // conflict-free and any lane can read the owner's row directly:
     //   pair slot s: fields 3s (gx), 3s+1 (gy), 3s+2 (rhs); walls: 3MP+w;
-    //   obstacle slot t: 3MP+4+3t (gx), +1 (gy), +2 (rhs)
-    static constexpr int kFields = 3 * MP + 4 + 3 * MO;
+    //   obstacle slot t: 3MP+4+3t (gx), +1 (gy), +2 (rhs); then the lanes' current
+    //   (ux, uy), published once per scan for the pair rows (cheaper than shuffles)
+    static constexpr int kU = 3 * MP + 4 + 3 * MO;
+    static constexpr int kFields = kU + 2;
     Real* rc;
     int N, P, off_obs, off_box;
     int npair;
@@ -154,13 +156,17 @@ struct BarrierRows {
 
     __device__ __forceinline__ void scan(const Grp<L>& g, Real ux, Real uy, Real& worst, int& p) const {
         const int lane = g.lane;
+        F(kU, lane) = ux;
+        F(kU + 1, lane) = uy;
+        Grp<L>::sync();
 #pragma unroll
         for (int s = 0; s < MP; ++s) {
-            const Real uxi = g.shfl(ux, pi[s]), uyi = g.shfl(uy, pi[s]);
-            const Real uxj = g.shfl(ux, pj[s]), uyj = g.shfl(uy, pj[s]);
-            if (s < npair && off(s))
+            if (s < npair && off(s)) {
+                const Real uxi = F(kU, pi[s]), uyi = F(kU + 1, pi[s]);
+                const Real uxj = F(kU, pj[s]), uyj = F(kU + 1, pj[s]);
                 consider(F(3 * s, lane) * (uxj - uxi) + F(3 * s + 1, lane) * (uyj - uyi) - F(3 * s + 2, lane),
                          lane + s * L, worst, p);
+            }
         }
         if (valid) {
             const int w0 = P + 4 * lane;
@@ -392,7 +398,7 @@ struct GroupSmem {
     QpWs<Real, BarrierDesc<Real>> qp;
     Real *xs, *ys, *ts, *tf, *rc;
     int *ti, *misc, *drones;
-    static __host__ __device__ int rc_reals(int L, int MP, int MO) { return (3 * MP + 4 + 3 * MO) * L; }
+    static __host__ __device__ int rc_reals(int L, int MP, int MO) { return (3 * MP + 4 + 3 * MO + 2) * L; }
     static __host__ __device__ int bytes(int N, int nf, int ni, int L, int MP, int MO) {
         const int qb = (QpWs<Real, BarrierDesc<Real>>::bytes(2 * N) + 15) & ~15;
         const int reals = 3 * N + nf + rc_reals(L, MP, MO);
