@@ -332,10 +332,14 @@ __device__ __forceinline__ int barrier_filter(const Grp<L>& g, BarrierRows<Real,
     if (!rows.valid) ux = uy = Real(0);
     // pair rows at the projected points (barrier.hpp:69-83 + fold_rows qp.hpp:104-125)
     bool coincident = false;
+    constexpr int kU = BarrierRows<Real, L, MP, MO>::kU;  // publish the projected points (smem, not shuffles)
+    rows.F(kU, lane) = prx;
+    rows.F(kU + 1, lane) = pry;
+    Grp<L>::sync();
 #pragma unroll
     for (int s = 0; s < MP; ++s) {
-        const Real xi = g.shfl(prx, rows.pi[s]), yi = g.shfl(pry, rows.pi[s]);
-        const Real xj = g.shfl(prx, rows.pj[s]), yj = g.shfl(pry, rows.pj[s]);
+        const Real xi = rows.F(kU, rows.pi[s]), yi = rows.F(kU + 1, rows.pi[s]);
+        const Real xj = rows.F(kU, rows.pj[s]), yj = rows.F(kU + 1, rows.pj[s]);
         const Real dx = xi - xj, dy = yi - yj;
         const Real dist2 = dx * dx + dy * dy;
         if (s < rows.npair && dist2 < Real(1e-18)) coincident = true;
@@ -436,16 +440,15 @@ __device__ __forceinline__ Real wrap_angle_dev(Real t) {
 // The fused step kernel. Persistent grid-stride loop; each warp steps 32/L
 // environments in lockstep (ghost groups past the end compute but never store).
 // ---------------------------------------------------------------------------
-// First-row QP fast path (qp_solve FAST): a measured per-task choice (B200,
-// fp64). It wins where most filtered steps enter one row from an empty active
-// set (navigation +8%, warehouse +10%, foraging +4%); elsewhere the extra code
-// costs more than it saves (predator_prey -4%, rware -10% at the old register
-// budget) or is neutral (N = 10 teams).
-__host__ __device__ constexpr bool qp_fast_first_row(int task) {
+// First-row QP fast path (qp_solve FAST): a measured choice (B200, fp64). It
+// pays for groups of 4 (teams of up to 4 robots: navigation +6%, warehouse +7%,
+// foraging +4%, rware neutral) and costs 2-4% for L = 8 (discovery / foraging
+// N = 6); L = 16 is neutral.
+__host__ __device__ constexpr bool qp_fast_first_row(int L) {
 #ifdef MRSIM_QP_NO_FAST
-    return false && task;
+    return false && L;
 #endif
-    return task != MRSIM_TASK_RWARE && task != MRSIM_TASK_PREDATOR_PREY && task != MRSIM_TASK_MATERIAL_TRANSPORT && task != MRSIM_TASK_ARCTIC_TRANSPORT;
+    return L == 4;
 }
 
 template <class Real, int L, int MP, int MO, int TASK>
@@ -574,7 +577,7 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
             }
             Real cv = nv, cw = nw;
             if (c.barrier_enabled) {
-                const int bs = barrier_filter<Real, L, MP, MO, qp_fast_first_row(TASK)>(g, rows, sm.qp, p.k, !skip, prx, pry, cs, sn, nv, nw,
+                const int bs = barrier_filter<Real, L, MP, MO, qp_fast_first_row(L)>(g, rows, sm.qp, p.k, !skip, prx, pry, cs, sn, nv, nw,
                                                        total_rows, cv, cw);
                 if (bs < 0 && !skip) {
                     if (lane == 0) {
@@ -599,10 +602,15 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
             // collision check (batch.hpp:204-209)
             if (N > 1) {  // squared distances; sqrt is monotone, so it is taken once per step
                 Real md2 = Consts<Real>::inf;
+                constexpr int kU = BarrierRows<Real, L, MP, MO>::kU;  // publish the poses (smem, not shuffles)
+                Grp<L>::sync();
+                rows.F(kU, lane) = x;
+                rows.F(kU + 1, lane) = y;
+                Grp<L>::sync();
 #pragma unroll
                 for (int s = 0; s < MP; ++s) {
-                    const Real xi = g.shfl(x, rows.pi[s]), yi = g.shfl(y, rows.pi[s]);
-                    const Real xj = g.shfl(x, rows.pj[s]), yj = g.shfl(y, rows.pj[s]);
+                    const Real xi = rows.F(kU, rows.pi[s]), yi = rows.F(kU + 1, rows.pi[s]);
+                    const Real xj = rows.F(kU, rows.pj[s]), yj = rows.F(kU + 1, rows.pj[s]);
                     const Real dx = xi - xj, dy = yi - yj;
                     if (s < rows.npair) md2 = dmin(md2, dx * dx + dy * dy);
                 }
