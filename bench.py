@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--dist-backend", default="nccl", help="nccl (GPUs) or gloo (multi-rank smoke test)")
+    ap.add_argument("--controller", default="unicycle_position", choices=["unicycle_position", "unicycle_pose"],
+                    help="ControllerKind (framework.hpp:126)")
     return ap.parse_args()
 
 
@@ -68,7 +70,9 @@ def dist_env():
 
 
 def workload_name(a) -> str:
-    return f"{a.task} N={a.robots}, {a.envs} envs/GPU, {a.max_steps}-step episodes, CBF on, random actions"
+    ctl = "" if a.controller == "unicycle_position" else ", pose controller"
+    acts = "stored random waypoints" if a.task == "random_waypoints" else "random actions"
+    return f"{a.task} N={a.robots}, {a.envs} envs/GPU, {a.max_steps}-step episodes, CBF on{ctl}, {acts}"
 
 
 def build_cfg(a):
@@ -80,6 +84,7 @@ def build_cfg(a):
     if a.task == "arctic_transport" and a.robots > 4:
         cfg.set_layout("arctic.spawn_zone", ARCTIC_SPAWN)
     cfg.max_steps = a.max_steps
+    cfg.set_controller(a.controller)
     cfg.validate()
     return cfg
 
@@ -91,7 +96,7 @@ def ref_spec(a):
     layout = {"arctic.spawn_zone": ARCTIC_SPAWN} if a.task == "arctic_transport" and a.robots > 4 else {}
     tile = a.task in ("discovery", "foraging", "material_transport", "arctic_transport", "warehouse")
     return refbind, refbind.spec(a.task, num_robots=a.robots, tile_roster=tile, max_steps=a.max_steps,
-                                 layout=layout)
+                                 layout=layout, controller=0 if a.controller == "unicycle_position" else 1)
 
 
 def cpu_reference_rate(a, seconds: float, max_envs: int):

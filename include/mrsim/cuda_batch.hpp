@@ -210,6 +210,12 @@ inline mrsim_env_state to_record(const EnvState& s) {
                 for (std::size_t k = 0; k < st.tiles.size(); ++k) o.tiles[k] = static_cast<int8_t>(st.tiles[k]);
             } else if constexpr (std::is_same_v<T, WarehouseState>) {
                 for (std::size_t k = 0; k < st.loaded.size(); ++k) o.loaded[k] = st.loaded[k] != 0;
+            } else if constexpr (std::is_same_v<T, RandomWaypointState>) {
+                for (std::size_t k = 0; k < st.targets.size(); ++k) {
+                    o.targets[k][0] = st.targets[k].x;
+                    o.targets[k][1] = st.targets[k].y;
+                    o.target_headings[k] = st.target_headings[k];
+                }
             }
         },
         s.scenario);
@@ -285,6 +291,15 @@ inline EnvState from_record(const mrsim_env_state& o, const ScenarioConfig& cfg)
             st.rows = o.rows;
             st.goal_zone = {o.goal_zone[0], o.goal_zone[1], o.goal_zone[2], o.goal_zone[3]};
             st.tiles.assign(o.tiles, o.tiles + o.cols * o.rows);
+            s.scenario = st;
+            break;
+        }
+        case MRSIM_TASK_RANDOM_WAYPOINTS: {
+            RandomWaypointState st;
+            for (int i = 0; i < n; ++i) {
+                st.targets.push_back({o.targets[i][0], o.targets[i][1]});
+                st.target_headings.push_back(o.target_headings[i]);
+            }
             s.scenario = st;
             break;
         }

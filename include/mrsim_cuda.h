@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define MRSIM_ABI_VERSION 1
+#define MRSIM_ABI_VERSION 2
 
 /* ---- return codes ---- */
 #define MRSIM_OK 0
@@ -47,7 +47,7 @@ extern "C" {
 #define MRSIM_MAX_TILES 128     /* arctic.grid_cols * arctic.grid_rows */
 #define MRSIM_MAX_HET_COLS 4
 
-/* ---- tasks (scenarios/all.hpp:17-30; random_waypoints is out of scope) ---- */
+/* ---- tasks (scenarios/all.hpp:17-30) ---- */
 #define MRSIM_TASK_NAVIGATION 0
 #define MRSIM_TASK_PREDATOR_PREY 1
 #define MRSIM_TASK_DISCOVERY 2
@@ -56,7 +56,8 @@ extern "C" {
 #define MRSIM_TASK_MATERIAL_TRANSPORT 5
 #define MRSIM_TASK_ARCTIC_TRANSPORT 6
 #define MRSIM_TASK_WAREHOUSE 7
-#define MRSIM_NUM_TASKS 8
+#define MRSIM_TASK_RANDOM_WAYPOINTS 8   /* throughput/determinism workload (random_waypoints.hpp) */
+#define MRSIM_NUM_TASKS 9
 
 /* ---- reward coefficient slots (ScenarioConfig::reward_coefficients, framework.hpp:139-151) ---- */
 #define MRSIM_COEF_VIOLATION 0
@@ -78,9 +79,10 @@ extern "C" {
 #define MRSIM_HET_OBS_OWN 1
 #define MRSIM_HET_OBS_FULL_TEAM 2
 
-/* ControllerKind (framework.hpp:126). Only the position controller is on the
- * device path (every benchmark scenario uses it); the pose controller is
- * rejected with MRSIM_E_UNSUPPORTED. */
+/* ControllerKind (framework.hpp:126): the projected-point position controller
+ * (controllers.hpp:86-92, every benchmark scenario's default) or the polar
+ * pose controller (controllers.hpp:68-82) with per-robot goal headings
+ * (Scenario::waypoint_headings, scenario.hpp:168-177). */
 #define MRSIM_CONTROLLER_UNICYCLE_POSITION 0
 #define MRSIM_CONTROLLER_UNICYCLE_POSE 1
 
@@ -192,6 +194,9 @@ typedef struct mrsim_env_state {
     int8_t tiles[MRSIM_MAX_TILES];
     /* warehouse */
     uint8_t loaded[MRSIM_MAX_ROBOTS];
+    /* random_waypoints (RandomWaypointState, scenario.hpp:66-69) */
+    double targets[MRSIM_MAX_ROBOTS][2];
+    double target_headings[MRSIM_MAX_ROBOTS];
 } mrsim_env_state;
 
 /* Per-device partial episode statistics (EpisodeStats/RunSummary,

@@ -331,6 +331,19 @@ static cmd_t position_controller(const mrsim_cfg* p, double x, double y, double 
     return clamp_command(cmd, p);
 }
 
+/* unicycle_pose_controller (controllers.hpp:68-82) */
+static cmd_t pose_controller(const mrsim_cfg* p, double x, double y, double th, double gx, double gy, double gth) {
+    const double dx = gx - x, dy = gy - y;
+    const double rho = hypot(dx, dy);
+    const double herr = wrap_angle(gth - th);
+    cmd_t zero = {0.0, 0.0};
+    if (rho < p->pose_position_tolerance && fabs(herr) < p->pose_heading_tolerance) return zero;
+    const double alpha = wrap_angle(atan2(dy, dx) - th);
+    const double beta = wrap_angle(gth - th - alpha);
+    cmd_t cmd = {p->k_rho * rho, p->k_alpha * alpha + p->k_beta * beta};
+    return clamp_command(cmd, p);
+}
+
 int orc_apply_barrier(const mrsim_cfg* p, int n, const double* poses, const double* nominal, int nobs,
                       const double* obstacles, const uint64_t* masks, double* commands, int* infeasible) {
     cmd_t out[MAXN];
@@ -463,6 +476,7 @@ int orc_obs_dim(const mrsim_cfg* c) {
             break;
         }
         case MRSIM_TASK_WAREHOUSE: d = base + 1; break;
+        case MRSIM_TASK_RANDOM_WAYPOINTS: d = 5; break;
     }
     if (c->het_obs_mode == MRSIM_HET_OBS_OWN) d += c->het_cols;
     else if (c->het_obs_mode == MRSIM_HET_OBS_FULL_TEAM) d += c->het_rows * c->het_cols;
@@ -505,6 +519,15 @@ static int arctic_tile_at(const mrsim_cfg* c, const mrsim_env_state* s, double x
     cc = (int)clampd(cc, 0, s->cols - 1);
     rr = (int)clampd(rr, 0, s->rows - 1);
     return s->tiles[rr * s->cols + cc];
+}
+
+/* RandomWaypointsScenario::draw_target + heading draw (random_waypoints.hpp:24-27, 34-35, 62-63) */
+static void rwp_draw(const mrsim_cfg* c, rng_t* rng, mrsim_env_state* s, int i) {
+    const double m = c->layout.rwp_waypoint_margin;
+    const double hw = c->arena_half_width, hh = c->arena_half_height;
+    s->targets[i][0] = uniform(rng, -hw + m, hw - m);
+    s->targets[i][1] = uniform(rng, -hh + m, hh - m);
+    s->target_headings[i] = PI * (1.0 - 2.0 * uniform01(rng));
 }
 
 int orc_reset_env(const mrsim_cfg* c, uint64_t seed, mrsim_env_state* s, char* err, int errlen) {
@@ -629,6 +652,11 @@ int orc_reset_env(const mrsim_cfg* c, uint64_t seed, mrsim_env_state* s, char* e
                     s->tiles[r * s->cols + cc] = uniform_int(&rng, 2) == 0 ? 1 : 2;
             break;
         }
+        case MRSIM_TASK_RANDOM_WAYPOINTS: /* random_waypoints.hpp:29-37 */
+            for (int i = 0; i < N; ++i) {
+                rwp_draw(c, &rng, s, i);
+            }
+            break;
         default:
             break;
     }
@@ -640,6 +668,18 @@ static double transition(const mrsim_cfg* c, mrsim_env_state* s, rng_t* rng) {
     const int N = c->num_robots;
     const mrsim_layout* y = &c->layout;
     switch (c->task) {
+        case MRSIM_TASK_RANDOM_WAYPOINTS: { /* random_waypoints.hpp:52-66 (sequential over robots) */
+            for (int i = 0; i < N; ++i) {
+                double cx = s->x[i], cy = s->y[i];
+                if (c->controller == MRSIM_CONTROLLER_UNICYCLE_POSITION) { /* projected_point */
+                    cx = s->x[i] + cos(s->theta[i]) * c->projection_distance;
+                    cy = s->y[i] + sin(s->theta[i]) * c->projection_distance;
+                }
+                if (hypot(cx - s->targets[i][0], cy - s->targets[i][1]) <= y->rwp_arrival_tolerance)
+                    rwp_draw(c, rng, s, i);
+            }
+            return 0.0;
+        }
         case MRSIM_TASK_NAVIGATION: { /* navigation.hpp:77-83 */
             double total = 0.0;
             for (int i = 0; i < N; ++i) total += hypot(s->x[i] - s->goals[i][0], s->y[i] - s->goals[i][1]);
@@ -848,7 +888,13 @@ int orc_observe(const mrsim_cfg* c, const mrsim_env_state* s, double* obs) {
     for (int r = 0; r < N; ++r) {
         double* o = obs + r * D;
         int q = 0;
-        if (c->task == MRSIM_TASK_NAVIGATION) { /* navigation.hpp:96-102 */
+        if (c->task == MRSIM_TASK_RANDOM_WAYPOINTS) { /* random_waypoints.hpp:70-76 */
+            o[q++] = s->x[r];
+            o[q++] = s->y[r];
+            o[q++] = s->theta[r];
+            o[q++] = s->targets[r][0];
+            o[q++] = s->targets[r][1];
+        } else if (c->task == MRSIM_TASK_NAVIGATION) { /* navigation.hpp:96-102 */
             o[q++] = s->x[r];
             o[q++] = s->y[r];
             o[q++] = s->theta[r];
@@ -956,14 +1002,28 @@ int orc_step_env(const mrsim_cfg* c, mrsim_env_state* s, const int32_t* actions,
         static const double DX[5] = {0.0, 0.0, 0.0, -1.0, 1.0}, DY[5] = {0.0, 1.0, -1.0, 0.0, 0.0};
         double px = s->x[i] + DX[actions[i]] * size;
         double py = s->y[i] + DY[actions[i]] * size;
-        if (c->action_noise_scale > 0.0) {
+        if (c->action_noise_scale > 0.0 && c->task != MRSIM_TASK_RANDOM_WAYPOINTS) {
             double half = c->action_noise_scale * size;
             px += uniform(&rng, -half, half);
             py += uniform(&rng, -half, half);
         }
         wx[i] = clampd(px, -c->arena_half_width, c->arena_half_width);
         wy[i] = clampd(py, -c->arena_half_height, c->arena_half_height);
+        if (c->task == MRSIM_TASK_RANDOM_WAYPOINTS) { /* actions ignored (random_waypoints.hpp:40-44) */
+            wx[i] = s->targets[i][0];
+            wy[i] = s->targets[i][1];
+        }
     }
+    double wth[MAXN]; /* waypoint_headings for the pose controller (batch.hpp:169-171) */
+    if (c->controller == MRSIM_CONTROLLER_UNICYCLE_POSE)
+        for (int i = 0; i < N; ++i) {
+            if (c->task == MRSIM_TASK_RANDOM_WAYPOINTS) { /* random_waypoints.hpp:46-50 */
+                wth[i] = s->target_headings[i];
+            } else { /* scenario.hpp:168-177 */
+                double dx = wx[i] - s->x[i], dy = wy[i] - s->y[i];
+                wth[i] = hypot(dx, dy) > 1e-12 ? atan2(dy, dx) : s->theta[i];
+            }
+        }
     /* add_obstacles (rware.hpp:54-68) */
     double obst[MRSIM_MAX_SLOTS * 3];
     uint64_t masks[MRSIM_MAX_SLOTS];
@@ -988,7 +1048,11 @@ int orc_step_env(const mrsim_cfg* c, mrsim_env_state* s, const int32_t* actions,
             poses[3 * i] = s->x[i];
             poses[3 * i + 1] = s->y[i];
             poses[3 * i + 2] = s->theta[i];
-            if (wx[i] == s->x[i] && wy[i] == s->y[i]) {
+            if (c->controller == MRSIM_CONTROLLER_UNICYCLE_POSE) {
+                cmd_t k = pose_controller(c, s->x[i], s->y[i], s->theta[i], wx[i], wy[i], wth[i]);
+                nom[2 * i] = k.v;
+                nom[2 * i + 1] = k.w;
+            } else if (wx[i] == s->x[i] && wy[i] == s->y[i]) {
                 nom[2 * i] = 0.0;
                 nom[2 * i + 1] = 0.0;
             } else {

@@ -32,7 +32,7 @@ struct RefSpec {
     int32_t max_steps;    // <= 0: task default
     int32_t sub_steps;    // <= 0: default
     int32_t barrier;      // -1 default, 0 off, 1 on
-    int32_t _pad;
+    int32_t controller;   // -1 default, else MRSIM_CONTROLLER_*
     double noise;         // < 0: default
     const char* layout;   // "key v v v;key2 v ..." overrides, may be NULL
 };
@@ -103,6 +103,9 @@ ScenarioConfig make_cfg(const RefSpec& s) {
     if (s.sub_steps > 0) cfg.sub_steps = s.sub_steps;
     if (s.noise >= 0) cfg.action_noise_scale = s.noise;
     if (s.barrier >= 0) cfg.barrier_enabled = s.barrier != 0;
+    if (s.controller >= 0)  // harness.hpp:95-96
+        cfg.controller = s.controller == MRSIM_CONTROLLER_UNICYCLE_POSE ? ControllerKind::UnicyclePose
+                                                                        : ControllerKind::UnicyclePosition;
     cfg.validate();
     return cfg;
 }
@@ -110,7 +113,7 @@ ScenarioConfig make_cfg(const RefSpec& s) {
 int task_id(const std::string& name) {
     static const char* names[] = {"navigation", "predator_prey", "discovery", "rware",
                                   "foraging", "material_transport", "arctic_transport",
-                                  "warehouse"};
+                                  "warehouse", "random_waypoints"};
     for (int i = 0; i < MRSIM_NUM_TASKS; ++i)
         if (name == names[i]) return i;
     return -1;
@@ -285,6 +288,12 @@ void to_flat(const EnvState& s, std::uint64_t seed, mrsim_env_state* o) {
             } else if constexpr (std::is_same_v<T, WarehouseState>) {
                 for (std::size_t k = 0; k < st.loaded.size() && k < MRSIM_MAX_ROBOTS; ++k)
                     o->loaded[k] = st.loaded[k] ? 1 : 0;
+            } else if constexpr (std::is_same_v<T, RandomWaypointState>) {
+                for (std::size_t k = 0; k < st.targets.size() && k < MRSIM_MAX_ROBOTS; ++k) {
+                    o->targets[k][0] = st.targets[k].x;
+                    o->targets[k][1] = st.targets[k].y;
+                    o->target_headings[k] = st.target_headings[k];
+                }
             }
         },
         s.scenario);
@@ -366,6 +375,15 @@ void from_flat(const mrsim_env_state* o, const ScenarioConfig& cfg, EnvState& s)
         case MRSIM_TASK_WAREHOUSE: {
             WarehouseState st;
             for (int k = 0; k < n; ++k) st.loaded.push_back(static_cast<char>(o->loaded[k]));
+            s.scenario = st;
+            break;
+        }
+        case MRSIM_TASK_RANDOM_WAYPOINTS: {
+            RandomWaypointState st;
+            for (int k = 0; k < n; ++k) {
+                st.targets.push_back({o->targets[k][0], o->targets[k][1]});
+                st.target_headings.push_back(o->target_headings[k]);
+            }
             s.scenario = st;
             break;
         }

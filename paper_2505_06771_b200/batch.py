@@ -23,7 +23,7 @@ from . import _abi
 from ._lib import InvalidArgument, lib, raise_for
 
 TASKS = ("navigation", "predator_prey", "discovery", "rware", "foraging", "material_transport",
-         "arctic_transport", "warehouse")
+         "arctic_transport", "warehouse", "random_waypoints")
 COEF_NAMES = ("violation", "dist", "tag", "sense", "step", "dropoff", "forage", "load", "delivery")
 
 
@@ -61,6 +61,14 @@ class ScenarioConfig:
             setattr(self.raw, key, value)
         else:
             object.__setattr__(self, key, value)
+
+    CONTROLLERS = ("unicycle_position", "unicycle_pose")  # ControllerKind names (harness.hpp:95-96, 117)
+
+    def set_controller(self, name: str) -> "ScenarioConfig":
+        if name not in self.CONTROLLERS:
+            raise InvalidArgument(f"unknown controller '{name}' (available: {', '.join(self.CONTROLLERS)})")
+        self.raw.controller = self.CONTROLLERS.index(name)
+        return self
 
     def coefficient(self, name: str) -> float:  # ScenarioConfig::coefficient (framework.hpp:145-151)
         k = COEF_NAMES.index(name)

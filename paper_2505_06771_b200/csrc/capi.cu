@@ -124,7 +124,8 @@ cudaError_t dispatch_step(int task, const StepParams<Real>& p, mrsim_host::Varia
         case 4: return launch_step<Real, 4>(p, v, grid, block, smem, s);
         case 5: return launch_step<Real, 5>(p, v, grid, block, smem, s);
         case 6: return launch_step<Real, 6>(p, v, grid, block, smem, s);
-        default: return launch_step<Real, 7>(p, v, grid, block, smem, s);
+        case 7: return launch_step<Real, 7>(p, v, grid, block, smem, s);
+        default: return launch_step<Real, 8>(p, v, grid, block, smem, s);
     }
 }
 template <class Real>
@@ -138,7 +139,8 @@ cudaError_t dispatch_occ(int task, mrsim_host::Variant v, int block, int smem, i
         case 4: return step_occupancy<Real, 4>(v, block, smem, bps);
         case 5: return step_occupancy<Real, 5>(v, block, smem, bps);
         case 6: return step_occupancy<Real, 6>(v, block, smem, bps);
-        default: return step_occupancy<Real, 7>(v, block, smem, bps);
+        case 7: return step_occupancy<Real, 7>(v, block, smem, bps);
+        default: return step_occupancy<Real, 8>(v, block, smem, bps);
     }
 }
 template <class Real>
@@ -152,7 +154,8 @@ cudaError_t dispatch_reset(int task, const ResetParams<Real>& p, cudaStream_t s)
         case 4: return launch_reset<Real, 4>(p, s);
         case 5: return launch_reset<Real, 5>(p, s);
         case 6: return launch_reset<Real, 6>(p, s);
-        default: return launch_reset<Real, 7>(p, s);
+        case 7: return launch_reset<Real, 7>(p, s);
+        default: return launch_reset<Real, 8>(p, s);
     }
 }
 
@@ -170,7 +173,8 @@ cudaError_t dispatch_observe(mrsim_ctx* ctx, const DevState<Real>& s, float* obs
         case 4: return launch_observe<Real, 4>(c, s, obs, B, D, bd, nf, ni, st);
         case 5: return launch_observe<Real, 5>(c, s, obs, B, D, bd, nf, ni, st);
         case 6: return launch_observe<Real, 6>(c, s, obs, B, D, bd, nf, ni, st);
-        default: return launch_observe<Real, 7>(c, s, obs, B, D, bd, nf, ni, st);
+        case 7: return launch_observe<Real, 7>(c, s, obs, B, D, bd, nf, ni, st);
+        default: return launch_observe<Real, 8>(c, s, obs, B, D, bd, nf, ni, st);
     }
 }
 
@@ -391,6 +395,13 @@ void to_host_states(mrsim_ctx* ctx, const DevState<Real>& s, long long first, lo
             case MRSIM_TASK_WAREHOUSE:
                 for (int i = 0; i < N; ++i) o.loaded[i] = (TI(0) >> i) & 1;
                 break;
+            case MRSIM_TASK_RANDOM_WAYPOINTS:
+                for (int i = 0; i < N; ++i) {
+                    o.targets[i][0] = TF(2 * i);
+                    o.targets[i][1] = TF(2 * i + 1);
+                    o.target_headings[i] = TF(2 * N + i);
+                }
+                break;
         }
     }
 }
@@ -482,6 +493,13 @@ void from_host_states(mrsim_ctx* ctx, const DevState<Real>& s, long long first, 
                 TI(0, lm);
                 break;
             }
+            case MRSIM_TASK_RANDOM_WAYPOINTS:
+                for (int i = 0; i < N; ++i) {
+                    TF(2 * i, o.targets[i][0]);
+                    TF(2 * i + 1, o.targets[i][1]);
+                    TF(2 * N + i, o.target_headings[i]);
+                }
+                break;
         }
     }
     cudaError_t e = cudaSuccess;

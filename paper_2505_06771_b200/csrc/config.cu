@@ -23,7 +23,7 @@ namespace {
 
 const char* kTaskNames[MRSIM_NUM_TASKS] = {"navigation", "predator_prey", "discovery", "rware",
                                            "foraging", "material_transport", "arctic_transport",
-                                           "warehouse"};
+                                           "warehouse", "random_waypoints"};
 
 void set4(double* d, double a, double b, double c, double e) {
     d[0] = a; d[1] = b; d[2] = c; d[3] = e;
@@ -227,6 +227,10 @@ int mrsim_config_default(const char* scenario, mrsim_cfg* out) {
             set_coef(&c, MRSIM_COEF_DELIVERY, 3.0);
             break;
         }
+        case MRSIM_TASK_RANDOM_WAYPOINTS:  // random_waypoints.hpp:15-21
+            steps(4, 0.2);
+            c.max_steps = 1000;
+            break;
     }
     set_coef(&c, MRSIM_COEF_VIOLATION, 0.0);
     return MRSIM_OK;
@@ -338,6 +342,8 @@ int mrsim_config_validate(const mrsim_cfg* cp, char* msg, int len) {
     if (c.num_robots < 1) return fail(msg, len, "ScenarioConfig: num_robots must be >= 1", IA);
     if (c.max_steps <= 0) return fail(msg, len, "ScenarioConfig: max_steps must be > 0", IA);
     if (c.sub_steps <= 0) return fail(msg, len, "ScenarioConfig: sub_steps must be > 0", IA);
+    if (c.controller != MRSIM_CONTROLLER_UNICYCLE_POSITION && c.controller != MRSIM_CONTROLLER_UNICYCLE_POSE)
+        return fail(msg, len, "ScenarioConfig: unknown controller", IA);
     if (c.action_noise_scale < 0) return fail(msg, len, "ScenarioConfig: action_noise_scale must be >= 0", IA);
     if (c.dt <= 0 || c.v_max <= 0 || c.omega_max <= 0 || c.si_max_speed <= 0 || c.arena_half_width <= 0 ||
         c.arena_half_height <= 0 || c.collision_radius <= 0)
@@ -391,8 +397,6 @@ int mrsim_config_validate(const mrsim_cfg* cp, char* msg, int len) {
         return fail(msg, len, "discovery: heterogeneity rows need [sense, tag]", IA);
     // Device-path capacity.
     if (c.num_robots > MRSIM_MAX_ROBOTS) return fail(msg, len, "device path supports num_robots <= 16", US);
-    if (c.controller != MRSIM_CONTROLLER_UNICYCLE_POSITION)
-        return fail(msg, len, "device path implements the unicycle position controller only", US);
     if (c.het_cols > MRSIM_MAX_HET_COLS) return fail(msg, len, "device path supports <= 4 heterogeneity columns", US);
     if (y.discovery_num_landmarks < 0 || y.discovery_num_landmarks > MRSIM_MAX_LANDMARKS)
         return fail(msg, len, "discovery.num_landmarks out of device range", US);

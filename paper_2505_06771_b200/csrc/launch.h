@@ -34,6 +34,11 @@ inline void fill_consts(const mrsim_cfg& c, mrsim_dev::PhysConsts<Real>& k) {
     k.obs_r_eff2 = Real(ro * ro);
     k.cap = Real(c.v_max + l * c.omega_max + 0.1);  // barrier.hpp:173
     k.tol = mrsim_dev::Prec<Real>::tol;
+    k.k_rho = Real(c.k_rho);
+    k.k_alpha = Real(c.k_alpha);
+    k.k_beta = Real(c.k_beta);
+    k.pose_ptol = Real(c.pose_position_tolerance);
+    k.pose_htol = Real(c.pose_heading_tolerance);
 }
 
 // Kernel variant for a config: L lanes per env (lane per robot), MP pair-row

@@ -59,6 +59,7 @@ template <class Real>
 struct PhysConsts {
     Real dt, v_max, w_max, si_max, hw, hh, coll_r, coll_r2, k_pos, l, inv_l, gamma, r_eff2, cap, obs_r_eff2, tol;
     Real wall_xmin, wall_xmax, wall_ymin, wall_ymax;
+    Real k_rho, k_alpha, k_beta, pose_ptol, pose_htol;  // pose controller (controllers.hpp:18-23)
 };
 
 template <class Real>
@@ -504,7 +505,12 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
         // ---- waypoints (Scenario::waypoints + action_to_waypoint) ----
         const uint64_t skey = fork_key(key, 1ull + static_cast<uint64_t>(step_index));  // step_stream
         Real wpx = x, wpy = y;
-        if (vl) {
+        if (TASK == MRSIM_TASK_RANDOM_WAYPOINTS) {  // actions ignored: the stored targets (random_waypoints.hpp:40-44)
+            if (vl) {
+                wpx = sm.tf[2 * ri];
+                wpy = sm.tf[2 * ri + 1];
+            }
+        } else if (vl) {
             const Real ss = step_size_of<TASK, Real>(c, sm.ti, ri, x, y);
             const Real dxa = (act == 3) ? Real(-1) : ((act == 4) ? Real(1) : Real(0));
             const Real dya = (act == 1) ? Real(1) : ((act == 2) ? Real(-1) : Real(0));
@@ -518,6 +524,18 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
             }
             wpx = dclamp(wpx, -p.k.hw, p.k.hw);
             wpy = dclamp(wpy, -p.k.hh, p.k.hh);
+        }
+
+        // goal headings for the pose controller (Scenario::waypoint_headings, batch.hpp:169-171)
+        const bool pose_ctl = c.controller == MRSIM_CONTROLLER_UNICYCLE_POSE;
+        Real wth = th;
+        if (pose_ctl) {
+            if (TASK == MRSIM_TASK_RANDOM_WAYPOINTS) {
+                wth = sm.tf[2 * N + ri];  // random_waypoints.hpp:46-50
+            } else {  // scenario.hpp:168-177
+                const Real ddx = wpx - x, ddy = wpy - y;
+                wth = dhypot(ddx, ddy) > Real(1e-12) ? atan2(ddy, ddx) : th;
+            }
         }
 
         // ---- static obstacles (Scenario::add_obstacles, rware.hpp:54-68) ----
@@ -563,7 +581,17 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
             const Real pry = y + sn * p.k.l;
             // nominal command (batch.hpp:183-191, controllers.hpp:39-55, 86-92)
             Real nv = 0, nw = 0;
-            if (!(wpx == x && wpy == y)) {
+            if (pose_ctl) {  // unicycle_pose_controller (controllers.hpp:68-82)
+                const Real dx = wpx - x, dy = wpy - y;
+                const Real rho = dhypot(dx, dy);
+                const Real herr = wrap_angle_dev(wth - th);
+                if (!(rho < p.k.pose_ptol && dabs(herr) < p.k.pose_htol)) {
+                    const Real alpha = wrap_angle_dev(atan2(dy, dx) - th);
+                    const Real beta = wrap_angle_dev(wth - th - alpha);
+                    nv = dclamp(p.k.k_rho * rho, -p.k.v_max, p.k.v_max);
+                    nw = dclamp(p.k.k_alpha * alpha + p.k.k_beta * beta, -p.k.w_max, p.k.w_max);
+                }
+            } else if (!(wpx == x && wpy == y)) {
                 Real ux = p.k.k_pos * (wpx - prx);
                 Real uy = p.k.k_pos * (wpy - pry);
                 const Real nrm = dsqrt(ux * ux + uy * uy);
@@ -633,7 +661,9 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
             int success = p.in.success[e];
             int collisions = p.in.collisions[e];
             Real ep_return = p.in.ep_return[e];
-            Rng trng{skey, c.action_noise_scale > 0.0 ? static_cast<uint64_t>(2 * N) : 0ull};
+            // the transition continues the step stream after the waypoint noise draws
+            Rng trng{skey, (c.action_noise_scale > 0.0 && TASK != MRSIM_TASK_RANDOM_WAYPOINTS)
+                               ? static_cast<uint64_t>(2 * N) : 0ull};
             EnvView<Real> v = view;
             Real reward = transition_task<TASK, Real>(c, v, trng, metric);
             if (collision) {

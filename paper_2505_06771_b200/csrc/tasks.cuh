@@ -1,7 +1,9 @@
 // tasks.cuh — the eight benchmark scenarios on the device: reset (fp64,
 // bit-exact draw order), step sizes, static obstacles, transition, finalize
 // and observation features. One set of functions per task, selected at
-// compile time by the TASK template parameter of the step kernel.
+// compile time by the TASK template parameter of the step kernel. The ninth
+// task, random_waypoints (random_waypoints.hpp), is the throughput workload
+// of the paper's Table 1 / Fig. 3.
 //
 // Reference: scenarios/*.hpp, scenario.hpp:93-130 (sample_poses, spawn
 // helpers), framework.hpp:61-76 (het_augment). Paths relative to
@@ -18,6 +20,7 @@
 //   material_transport TF: circle, rect, delivered, total_initial, loads[N]
 //   arctic_transport   TI bytes: tiles[cols*rows]
 //   warehouse          TI: loaded mask
+//   random_waypoints   TF: targets[2N], target_headings[N]
 #pragma once
 
 #include <cmath>
@@ -26,7 +29,7 @@
 
 namespace mrsim_dev {
 
-constexpr int kTfMax = 32;
+constexpr int kTfMax = 48;
 constexpr int kTiMax = 32;
 
 // Requests actually drawn at reset: min(request_size, num_shelves) (rware.hpp:38-42).
@@ -50,6 +53,7 @@ __host__ __device__ inline void task_fields(const mrsim_cfg& c, int* nf, int* ni
         case MRSIM_TASK_MATERIAL_TRANSPORT: *nf = 4 + N; break;
         case MRSIM_TASK_ARCTIC_TRANSPORT: *ni = (y.arctic_grid_cols * y.arctic_grid_rows + 3) / 4; break;
         case MRSIM_TASK_WAREHOUSE: *ni = 1; break;
+        case MRSIM_TASK_RANDOM_WAYPOINTS: *nf = 3 * N; break;
         default: break;
     }
 }
@@ -102,6 +106,15 @@ __device__ inline int sample_poses_dev(int n, double xmin, double xmax, double y
         }
     }
     return 0;
+}
+
+// RandomWaypointsScenario::draw_target + a heading (random_waypoints.hpp:24-27, 34-35, 62-63)
+__device__ __forceinline__ void rwp_draw(const mrsim_cfg& c, Rng& rng, double& tx, double& ty, double& th) {
+    const double m = c.layout.rwp_waypoint_margin;
+    const double hw = c.arena_half_width, hh = c.arena_half_height;
+    tx = rng.uniform(-hw + m, hw - m);
+    ty = rng.uniform(-hh + m, hh - m);
+    th = __dmul_rn(3.14159265358979323846, __dsub_rn(1.0, __dmul_rn(2.0, rng.uniform())));
 }
 
 template <int TASK>
@@ -219,6 +232,8 @@ __device__ inline int reset_task(const mrsim_cfg& c, uint64_t key, ResetOut& o, 
                 ti_set_byte(o.ti, r * cols + cc, rng.uniform_int(2) == 0 ? 1 : 2);
     } else if (TASK == MRSIM_TASK_WAREHOUSE) {
         o.ti[0] = 0;
+    } else if (TASK == MRSIM_TASK_RANDOM_WAYPOINTS) {  // random_waypoints.hpp:29-37
+        for (int i = 0; i < N; ++i) rwp_draw(c, rng, o.tf[2 * i], o.tf[2 * i + 1], o.tf[2 * N + i]);
     }
     return 0;
 }
@@ -469,6 +484,25 @@ __device__ Real transition_task(const mrsim_cfg& c, EnvView<Real>& v, Rng& rng, 
             all_in = all_in && rect_contains<Real>(gz, px, py);
         }
         return Real(c.coef[MRSIM_COEF_DIST]) * summed + Real(c.coef[MRSIM_COEF_STEP]) * (all_in ? Real(0) : Real(1));
+    } else if (TASK == MRSIM_TASK_RANDOM_WAYPOINTS) {  // random_waypoints.hpp:52-66 (sequential over robots)
+        const Real tol = Real(L.rwp_arrival_tolerance);
+        for (int i = 0; i < N; ++i) {
+            Real cx = v.xs[i], cy = v.ys[i];
+            if (c.controller == MRSIM_CONTROLLER_UNICYCLE_POSITION) {  // projected_point (controllers.hpp:34-36)
+                Real sn, cs;
+                dsincos(v.ts[i], &sn, &cs);
+                cx = v.xs[i] + cs * Real(c.projection_distance);
+                cy = v.ys[i] + sn * Real(c.projection_distance);
+            }
+            if (dhypot(cx - v.tf[2 * i], cy - v.tf[2 * i + 1]) <= tol) {
+                double tx, ty, th;
+                rwp_draw(c, rng, tx, ty, th);
+                v.tf[2 * i] = Real(tx);
+                v.tf[2 * i + 1] = Real(ty);
+                v.tf[2 * N + i] = Real(th);
+            }
+        }
+        return Real(0);
     } else {  // warehouse.hpp:36-54
         Real reward = 0;
         int loaded = v.ti[0];
@@ -530,6 +564,7 @@ __host__ __device__ inline int base_obs_dim(const mrsim_cfg& c) {
             return base + 1 + 9 * drones;
         }
         case MRSIM_TASK_WAREHOUSE: return base + 1;
+        case MRSIM_TASK_RANDOM_WAYPOINTS: return 5;
         default: return 0;
     }
 }
@@ -550,6 +585,15 @@ __device__ float obs_feature(const mrsim_cfg& c, const EnvView<Real>& v, int r, 
         const int k = q - bdim;
         if (c.het_obs_mode == MRSIM_HET_OBS_OWN) return static_cast<float>(c.het[r][k]);
         return static_cast<float>(c.het[k / c.het_cols][k % c.het_cols]);
+    }
+    if (TASK == MRSIM_TASK_RANDOM_WAYPOINTS) {  // random_waypoints.hpp:70-76: own pose + target
+        switch (q) {
+            case 0: return static_cast<float>(v.xs[r]);
+            case 1: return static_cast<float>(v.ys[r]);
+            case 2: return static_cast<float>(v.ts[r]);
+            case 3: return static_cast<float>(v.tf[2 * r]);
+            default: return static_cast<float>(v.tf[2 * r + 1]);
+        }
     }
     if (TASK == MRSIM_TASK_NAVIGATION) {  // navigation.hpp:96-102
         switch (q) {

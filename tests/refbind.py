@@ -21,7 +21,7 @@ P = ctypes.POINTER
 class RefSpec(ctypes.Structure):
     _fields_ = [("scenario", ctypes.c_char_p), ("num_robots", ctypes.c_int32), ("tile_roster", ctypes.c_int32),
                 ("max_steps", ctypes.c_int32), ("sub_steps", ctypes.c_int32), ("barrier", ctypes.c_int32),
-                ("_pad", ctypes.c_int32), ("noise", ctypes.c_double), ("layout", ctypes.c_char_p)]
+                ("controller", ctypes.c_int32), ("noise", ctypes.c_double), ("layout", ctypes.c_char_p)]
 
 
 _lib = None
@@ -85,9 +85,9 @@ def dptr(a: np.ndarray):
 
 
 def spec(scenario: str, num_robots: int = 0, tile_roster: bool = False, max_steps: int = 0, sub_steps: int = 0,
-         barrier: int = -1, noise: float = -1.0, layout: dict | None = None) -> RefSpec:
+         barrier: int = -1, noise: float = -1.0, layout: dict | None = None, controller: int = -1) -> RefSpec:
     text = ";".join(f"{k} " + " ".join(repr(float(v)) for v in vals) for k, vals in (layout or {}).items())
-    s = RefSpec(scenario.encode(), num_robots, int(tile_roster), max_steps, sub_steps, barrier, 0, noise,
+    s = RefSpec(scenario.encode(), num_robots, int(tile_roster), max_steps, sub_steps, barrier, controller, noise,
                 text.encode())
     s._keep = text  # noqa: keep the buffer alive
     return s

@@ -40,7 +40,7 @@ def test_default_config_matches_reference(task, ref):
 @pytest.mark.parametrize("task,n", [
     ("navigation", 4), ("discovery", 6), ("predator_prey", 6), ("rware", 4), ("rware", 6),
     ("foraging", 4), ("foraging", 6), ("material_transport", 10), ("arctic_transport", 10),
-    ("warehouse", 6), ("navigation", 16),
+    ("warehouse", 6), ("navigation", 16), ("random_waypoints", 8),
 ])
 def test_num_robots_and_roster_tiling_match_reference(task, n, ref):
     cfg = m.make_default_config(task)
@@ -75,6 +75,14 @@ def test_layout_overrides_match_reference(key, vals, ref):
     cfg.set_layout(key, vals)
     theirs = ref.resolve_config(ref.spec(task, layout={key: vals}))
     assert diff_structs(cfg.raw, theirs) == {}
+
+
+def test_pose_controller_config_matches_reference(ref):
+    for task in ("navigation", "random_waypoints", "rware"):
+        cfg = m.make_default_config(task).set_controller("unicycle_pose")
+        cfg.validate()
+        theirs = ref.resolve_config(ref.spec(task, controller=1))
+        assert diff_structs(cfg.raw, theirs) == {}
 
 
 def test_overrides_max_steps_barrier_noise(ref):
@@ -112,9 +120,11 @@ def test_validation_errors_mirror_reference():
     with pytest.raises(m.Unsupported):
         cfg.set_num_robots(17)
     cfg = m.make_default_config("navigation")
-    cfg.controller = 1
-    with pytest.raises(m.Unsupported, match="position controller"):
+    cfg.controller = 2
+    with pytest.raises(m.InvalidArgument, match="controller"):
         cfg.validate()
+    with pytest.raises(m.InvalidArgument, match="unknown controller"):
+        m.make_default_config("navigation").set_controller("pid")
     with pytest.raises(m.InvalidArgument):
         m.make_default_config("navigation").set_layout("no.such.key", [1.0])
 
@@ -123,7 +133,7 @@ def test_validation_errors_mirror_reference():
 def test_obs_dims_match_reference(task, ref):
     # test_framework.cpp:232-259 pins the default-N dimensions
     expected = {"arctic_transport": 31, "discovery": 29, "foraging": 16, "material_transport": 20,
-                "navigation": 5, "predator_prey": 9, "rware": 29, "warehouse": 12}
+                "navigation": 5, "predator_prey": 9, "rware": 29, "warehouse": 12, "random_waypoints": 5}
     assert m.make_default_config(task).obs_dim == expected[task]
     rb = ref.RefBatch(ref.spec(task))
     assert rb.D == expected[task]

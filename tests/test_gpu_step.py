@@ -28,11 +28,14 @@ pytestmark = pytest.mark.gpu
 # BASELINE.json configs 2-5 (+ warehouse at default N)
 CONFIGS = [("navigation", 4), ("predator_prey", 6), ("discovery", 6), ("rware", 4), ("rware", 6),
            ("foraging", 4), ("foraging", 6), ("material_transport", 10), ("arctic_transport", 10),
-           ("warehouse", 4)]
+           ("warehouse", 4), ("random_waypoints", 4)]
+# ControllerKind::UnicyclePose (controllers.hpp:68-82) on a subset, horizon capped at 150 steps
+POSE_CONFIGS = [("navigation", 4), ("random_waypoints", 4), ("random_waypoints", 10), ("rware", 4),
+                ("material_transport", 10)]
 ARCTIC_SPAWN = [-1.55, -1.05, -0.9, 0.9]  # default zone fails 1.4% of N=10 resets
 
 
-def make_cfgs(ref, task, n, max_steps=0):
+def make_cfgs(ref, task, n, max_steps=0, controller=-1):
     cfg = m.make_default_config(task)
     tile = cfg.raw.het_rows > 0
     if n != cfg.raw.num_robots:
@@ -43,7 +46,9 @@ def make_cfgs(ref, task, n, max_steps=0):
         layout["arctic.spawn_zone"] = ARCTIC_SPAWN
     if max_steps:
         cfg.max_steps = max_steps
-    sp = ref.spec(task, num_robots=n, tile_roster=tile, layout=layout, max_steps=max_steps)
+    if controller >= 0:
+        cfg.controller = controller
+    sp = ref.spec(task, num_robots=n, tile_roster=tile, layout=layout, max_steps=max_steps, controller=controller)
     return cfg, sp
 
 
@@ -69,7 +74,7 @@ def compare_states(a, b, N, pos_tol, ang_tol, real_tol):
         for f in ("scenario_metric", "circle_remaining", "rect_remaining", "delivered", "total_initial"):
             re_ = max(re_, abs(getattr(sa, f) - getattr(sb, f)))
         re_ = max(re_, float(np.max(np.abs(np.array(sa.loads[:N]) - np.array(sb.loads[:N])))))
-        for arr in ("goals", "landmarks", "resources", "prey"):
+        for arr in ("goals", "landmarks", "resources", "prey", "targets", "target_headings"):
             re_ = max(re_, float(np.max(np.abs(np.array(getattr(sa, arr)) - np.array(getattr(sb, arr))))))
     return pe, ae, bad, re_
 
@@ -98,8 +103,8 @@ def test_reset_matches_reference(task, n, fp64, ref):
         assert sa.rng_key == sb.rng_key
 
 
-def _teacher_forced(ref, task, n, fp64, sub_steps, T, B=48):
-    cfg, sp = make_cfgs(ref, task, n)
+def _teacher_forced(ref, task, n, fp64, sub_steps, T, B=48, max_steps=0, controller=-1):
+    cfg, sp = make_cfgs(ref, task, n, max_steps=max_steps, controller=controller)
     if sub_steps:
         cfg.sub_steps = sub_steps
         sp.sub_steps = sub_steps
@@ -139,6 +144,34 @@ def test_teacher_forced_steps_match_reference_fp64(task, n, ref):
     assert st["real"] <= 1e-9, st
     assert st["reward_bad"] == 0
     assert st["obs"] <= 2e-6 * 16  # fp32 obs of values up to |16|
+
+
+@pytest.mark.parametrize("task,n", POSE_CONFIGS)
+def test_teacher_forced_pose_controller_fp64(task, n, ref):
+    cfg, st = _teacher_forced(ref, task, n, True, 0, 152, max_steps=150, controller=1)
+    assert st["discrete"] == [], st["discrete"][:5]
+    assert st["pose"] <= 1e-9 and st["angle"] <= 1e-8, st
+    assert st["real"] <= 1e-9, st
+    assert st["reward_bad"] == 0
+
+
+@pytest.mark.parametrize("task,n", POSE_CONFIGS)
+def test_free_running_pose_controller_fp64(task, n, ref):
+    cfg, sp = make_cfgs(ref, task, n, max_steps=150, controller=1)
+    B = 64
+    seeds = [m.derive_episode_seed(4, e) for e in range(B)]
+    rb = ref.RefBatch(sp)
+    rb.reset(seeds)
+    gb = m.CudaEnvBatch(cfg, B, fp64=True)
+    gb.reset_seeds(seeds)
+    for t in range(150):
+        acts = rb.random_actions()
+        _, grew, gdone = gb.step_host(acts)
+        _, rrew, rdone, _ = rb.step(acts)
+        assert np.array_equal(gdone, rdone)
+        pe, ae, bad, re_ = compare_states(gb.get_states(), rb.get_states(), n, 0, 0, 0)
+        assert not bad and pe <= 1e-8 and ae <= 1e-7 and re_ <= 1e-8, (t, pe, ae, bad[:3], re_)
+        assert np.all(np.abs(grew - rrew) <= 1e-9 * np.maximum(1.0, np.abs(rrew)))
 
 
 @pytest.mark.parametrize("task,n", CONFIGS)

@@ -18,7 +18,7 @@ from util import diff_structs
 CONFIGS = [("navigation", 3), ("navigation", 4), ("predator_prey", 3), ("predator_prey", 6), ("discovery", 4),
            ("discovery", 6), ("rware", 3), ("rware", 4), ("rware", 6), ("foraging", 3), ("foraging", 4),
            ("foraging", 6), ("material_transport", 4), ("material_transport", 10), ("arctic_transport", 4),
-           ("arctic_transport", 10), ("warehouse", 4)]
+           ("arctic_transport", 10), ("warehouse", 4), ("random_waypoints", 4)]
 ARCTIC_SPAWN = [-1.55, -1.05, -0.9, 0.9]
 
 
@@ -44,7 +44,7 @@ def cfg_and_spec(ref, task, n, **kw):
         setattr(cfg.raw, k, v)
     sp = ref.spec(task, num_robots=n, tile_roster=tile, layout=layout,
                   max_steps=kw.get("max_steps", 0), barrier=kw.get("barrier_enabled", -1),
-                  noise=kw.get("action_noise_scale", -1.0))
+                  noise=kw.get("action_noise_scale", -1.0), controller=kw.get("controller", -1))
     return cfg, sp
 
 
@@ -135,6 +135,57 @@ def test_rollouts_bit_exact_against_reference(task, n, orc, ref):
             d = diff_structs(env.state, rs[e])
             d.pop("episode_return", None)
             assert d == {}, (t, e, d)
+
+
+@pytest.mark.parametrize("task,n", [("navigation", 4), ("rware", 4), ("random_waypoints", 4),
+                                    ("random_waypoints", 8), ("material_transport", 4)])
+def test_pose_controller_rollouts_bit_exact(task, n, orc, ref):
+    # ControllerKind::UnicyclePose (controllers.hpp:68-82, batch.hpp:169-195)
+    cfg, sp = cfg_and_spec(ref, task, n, controller=1, max_steps=120)
+    rb = ref.RefBatch(sp)
+    seeds = [m.derive_episode_seed(3, e) for e in range(4)]
+    robs = rb.reset(seeds)
+    envs = [orc.OracleEnv(cfg.raw) for _ in seeds]
+    for e, env in enumerate(envs):
+        assert np.array_equal(env.reset(seeds[e]), robs[e])
+    for t in range(120):
+        acts = rb.random_actions()
+        robs, rrew, rdone, _ = rb.step(acts)
+        rs = rb.get_states()
+        for e, env in enumerate(envs):
+            obs, rew, done = env.step(acts[e])
+            assert rew == rrew[e] and np.array_equal(obs, robs[e]), (t, e)
+            d = diff_structs(env.state, rs[e])
+            d.pop("episode_return", None)
+            assert d == {}, (t, e, d)
+
+
+def test_random_waypoints_reassignment_and_noise(orc, ref):
+    # test_scenario_rules.cpp:545-566: seed 99, all-stay, targets change within 100 steps
+    cfg = m.make_default_config("random_waypoints")
+    cfg.max_steps = 200
+    env = orc.OracleEnv(cfg.raw)
+    env.reset(99)
+    changes = 0
+    for _ in range(100):
+        before = np.array(env.state.targets)[:4].copy()
+        env.step([0] * 4)
+        changes += int(np.sum(np.any(np.array(env.state.targets)[:4] != before, axis=1)))
+    assert changes > 0
+    # waypoint noise must not consume draws for this task (its waypoints ignore the rng)
+    cfg2, sp = cfg_and_spec(ref, "random_waypoints", 4, action_noise_scale=0.3, max_steps=60)
+    rb = ref.RefBatch(sp)
+    rb.reset([1, 2])
+    envs = [orc.OracleEnv(cfg2.raw) for _ in range(2)]
+    for env, sd in zip(envs, [1, 2]):
+        env.reset(sd)
+    for t in range(60):
+        acts = rb.random_actions()
+        robs, rrew, _, _ = rb.step(acts)
+        rs = rb.get_states()
+        for e, env in enumerate(envs):
+            obs, rew, _ = env.step(acts[e])
+            assert np.array_equal(obs, robs[e]) and diff_structs(env.state, rs[e]).keys() <= {"episode_return"}
 
 
 def test_rollouts_with_noise_and_barrier_off(orc, ref):
