@@ -260,10 +260,11 @@ int mrsim_reset_episodes(mrsim_ctx* ctx, uint64_t root_seed, int64_t first_episo
                          int64_t episode_stride, float* obs_dev, void* stream);
 
 /* step_batch (batch.hpp:268-290) / step_env (batch.hpp:165-224) for every env.
- *   actions_dev : device int8 [num_envs][N] in 0..4, or NULL to draw them
- *                 on device with the harness random policy
- *                 policy_stream(seed_e, step, r).uniform_int(5)
- *                 (harness.hpp:29-34, policy.hpp:448-449)
+ *   actions_dev : device int8 [num_envs][N] in 0..4, or NULL to let the
+ *                 context's policy produce them on device: the harness random
+ *                 policy policy_stream(seed_e, step, r).uniform_int(5)
+ *                 (harness.hpp:29-34, policy.hpp:448-449) by default, or the
+ *                 feedforward network set by mrsim_set_policy_feedforward
  *   obs_dev     : device fp32 [num_envs][N][D] (terminal obs on a done step, as
  *                 the reference returns), may be NULL
  *   reward_dev  : device fp32 [num_envs] team reward, may be NULL
@@ -288,6 +289,30 @@ int mrsim_observe(mrsim_ctx* ctx, float* obs_dev, void* stream);
 int mrsim_observe_host(mrsim_ctx* ctx, float* obs_host);
 /* Draw the harness random-policy actions for the current step into actions_dev. */
 int mrsim_random_actions(mrsim_ctx* ctx, int8_t* actions_dev, void* stream);
+
+/* ---- on-device policy (Policy / PolicySpec, policy.hpp:17-57, 445-486) ---- */
+#define MRSIM_ACT_RELU 0      /* Activation (policy.hpp:60) */
+#define MRSIM_ACT_TANH 1
+#define MRSIM_ACT_IDENTITY 2
+#define MRSIM_POLICY_MAX_LAYERS 8
+#define MRSIM_POLICY_MAX_WIDTH 256
+/* PolicyKind::FeedforwardFile with the weights already parsed
+ * (FeedforwardWeights, policy.hpp:62-95; the text file format stays host
+ * side): layer l maps dims[2l] -> dims[2l+1] inputs -> outputs with
+ * activation[l]; `weights` holds, layer after layer, W (out x in, row-major,
+ * as DenseLayer::w) then b (out). greedy != 0: argmax of the logits, else a
+ * softmax sample from policy_stream (feedforward_sample:). Validates like
+ * FeedforwardWeights::validate (chained dims, 5 logits) plus input dim ==
+ * mrsim_obs_dim (forward's size check). Replaces the random policy used by
+ * mrsim_step(actions_dev = NULL). Synchronous. */
+int mrsim_set_policy_feedforward(mrsim_ctx* ctx, int num_layers, const int32_t* dims, const int32_t* activation,
+                                 const double* weights, int greedy);
+/* Back to PolicyKind::Random (the default). */
+int mrsim_set_policy_random(mrsim_ctx* ctx);
+/* The context policy's actions for the current step of every env (the
+ * observation of the current state, i.e. the one the last reset/step
+ * returned) into actions_dev [num_envs][N]. Asynchronous on `stream`. */
+int mrsim_policy_actions(mrsim_ctx* ctx, int8_t* actions_dev, void* stream);
 /* Wait for the context's work on `stream` and report sticky device errors. */
 int mrsim_sync(mrsim_ctx* ctx, void* stream);
 

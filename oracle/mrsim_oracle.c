@@ -1098,3 +1098,50 @@ int orc_step_env(const mrsim_cfg* c, mrsim_env_state* s, const int32_t* actions,
     if (obs) orc_observe(c, s, obs);
     return MRSIM_OK;
 }
+
+/* ---------------- feedforward policy (policy.hpp:95-116, 445-480) ---------------- */
+
+int orc_policy_act(const mrsim_cfg* c, const mrsim_env_state* s, int robot, int num_layers, const int32_t* dims,
+                   const int32_t* acts, const double* weights, int greedy) {
+    double obs[MAXN * 128], buf[2][256];
+    const int D = orc_obs_dim(c);
+    orc_observe(c, s, obs); /* assemble_observations (batch.hpp:143-151) */
+    for (int i = 0; i < D; ++i) buf[0][i] = obs[robot * D + i];
+    int cur = 0;
+    const double* w = weights;
+    for (int l = 0; l < num_layers; ++l) { /* FeedforwardWeights::forward */
+        const int in = dims[2 * l], out = dims[2 * l + 1];
+        const double* b = w + in * out;
+        for (int o = 0; o < out; ++o) {
+            double acc = b[o];
+            for (int i = 0; i < in; ++i) acc += w[o * in + i] * buf[cur][i];
+            if (acts[l] == MRSIM_ACT_RELU) acc = acc > 0 ? acc : 0;
+            else if (acts[l] == MRSIM_ACT_TANH) acc = tanh(acc);
+            buf[cur ^ 1][o] = acc;
+        }
+        w = b + out;
+        cur ^= 1;
+    }
+    const double* lg = buf[cur];
+    if (greedy) {
+        int best = 0;
+        for (int a = 1; a < 5; ++a)
+            if (lg[a] > lg[best]) best = a;
+        return best;
+    }
+    double mx = lg[0], p[5], z = 0.0;
+    for (int a = 0; a < 5; ++a) mx = dmax(mx, lg[a]);
+    for (int a = 0; a < 5; ++a) {
+        p[a] = exp(lg[a] - mx);
+        z += p[a];
+    }
+    /* policy_stream(seed, step, robot) (harness.hpp:29-34) */
+    rng_t rng = {orc_fork(orc_fork(orc_fork(orc_key_from_seed(s->seed), 0x9D0C7E5F00000001ULL), (uint64_t)s->step_index),
+                          (uint64_t)robot), 0};
+    double u = uniform01(&rng) * z;
+    for (int a = 0; a < 5; ++a) {
+        u -= p[a];
+        if (u <= 0.0) return a;
+    }
+    return 4;
+}

@@ -49,6 +49,10 @@ int orc_step_env(const mrsim_cfg* cfg, mrsim_env_state* st, const int32_t* actio
                  int* done, char* err, int errlen);
 /* assemble_observations (batch.hpp:143-151). */
 int orc_observe(const mrsim_cfg* cfg, const mrsim_env_state* st, double* obs);
+/* Policy::act for PolicyKind::FeedforwardFile (policy.hpp:445-480) on robot `robot`'s observation of
+ * the current state; layers packed as in mrsim_set_policy_feedforward. */
+int orc_policy_act(const mrsim_cfg* cfg, const mrsim_env_state* st, int robot, int num_layers, const int32_t* dims,
+                   const int32_t* acts, const double* weights, int greedy);
 
 #ifdef __cplusplus
 }

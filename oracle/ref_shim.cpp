@@ -559,6 +559,35 @@ int ref_random_actions(void* h, int32_t* out) {
     return 0;
 }
 
+// Policy::act (policy.hpp:445-480) for every robot of every env on the
+// current observation, seeded like run_episodes (harness.hpp:238-252).
+// spec: a PolicySpec string ("random", "feedforward:<path>", ...).
+int ref_policy_actions(void* h, const char* spec, int32_t* out, char* err, int errlen) {
+    try {
+        auto* b = static_cast<RefBatch*>(h);
+        const int n = b->cfg.num_robots;
+        Policy policy(PolicySpec::parse(spec));
+        PolicyContext ctx;
+        ctx.cfg = &b->cfg;
+        ctx.scenario = b->scenario.get();
+        for (int e = 0; e < b->state.size(); ++e) {
+            const EnvState& env = b->state.envs[static_cast<std::size_t>(e)];
+            const auto obs = assemble_observations(env, b->cfg, *b->scenario);
+            ctx.state = &env;
+            for (int r = 0; r < n; ++r) {
+                ctx.robot = r;
+                SplitRng prng = policy_stream(b->seeds[static_cast<std::size_t>(e)], env.step_index, r);
+                out[static_cast<std::size_t>(e) * n + r] =
+                    static_cast<int32_t>(policy.act(obs[static_cast<std::size_t>(r)], prng, ctx));
+            }
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        put_err(err, errlen, e);
+        return code_of(e);
+    }
+}
+
 // CPU baseline: time `steps` step_batch calls (harness.hpp:356-362 style,
 // steady_clock, setup excluded) with random-policy actions precomputed per step.
 double ref_time_steps(void* h, int steps) {

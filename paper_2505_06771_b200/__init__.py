@@ -7,11 +7,11 @@ mirror of the reference's reset_batch / step_batch / ScenarioConfig.
 """
 from ._lib import (CudaError, DomainError, InvalidArgument, MrsimError, SimRuntimeError, Unsupported,
                    lib)
-from .batch import (TASKS, CudaEnvBatch, ScenarioConfig, StepOutputs, derive_episode_seed,
+from .batch import (TASKS, CudaEnvBatch, FeedforwardWeights, ScenarioConfig, StepOutputs, derive_episode_seed,
                     make_default_config, reset_batch, step_batch)
 
 __all__ = [
-    "TASKS", "CudaEnvBatch", "ScenarioConfig", "StepOutputs", "make_default_config", "reset_batch",
+    "TASKS", "CudaEnvBatch", "FeedforwardWeights", "ScenarioConfig", "StepOutputs", "make_default_config", "reset_batch",
     "step_batch", "derive_episode_seed", "lib", "MrsimError", "InvalidArgument", "DomainError",
     "SimRuntimeError", "CudaError", "Unsupported",
 ]

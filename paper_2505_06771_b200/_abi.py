@@ -103,6 +103,10 @@ FUNCTIONS = {
     "mrsim_observe": (ctypes.c_int, [c_void_p, c_void_p, c_void_p]),
     "mrsim_observe_host": (ctypes.c_int, [c_void_p, P(ctypes.c_float)]),
     "mrsim_random_actions": (ctypes.c_int, [c_void_p, c_void_p, c_void_p]),
+    "mrsim_set_policy_feedforward": (ctypes.c_int, [c_void_p, ctypes.c_int, P(ctypes.c_int32), P(ctypes.c_int32),
+                                                    P(ctypes.c_double), ctypes.c_int]),
+    "mrsim_set_policy_random": (ctypes.c_int, [c_void_p]),
+    "mrsim_policy_actions": (ctypes.c_int, [c_void_p, c_void_p, c_void_p]),
     "mrsim_sync": (ctypes.c_int, [c_void_p, c_void_p]),
     "mrsim_get_env_states": (ctypes.c_int, [c_void_p, ctypes.c_int64, ctypes.c_int64, P(EnvState)]),
     "mrsim_set_env_states": (ctypes.c_int, [c_void_p, ctypes.c_int64, ctypes.c_int64, P(EnvState)]),

@@ -236,6 +236,37 @@ class CudaEnvBatch:
                                                _stream_handle(stream)))
         return self._actions
 
+    # -- on-device policy (Policy, policy.hpp:432-486) --
+    def set_policy(self, spec):
+        """PolicySpec forms (policy.hpp:24-47): "random", "feedforward:<path>",
+        "feedforward_sample:<path>", or a FeedforwardWeights (greedy)."""
+        if isinstance(spec, FeedforwardWeights):
+            return self.set_feedforward(spec, greedy=True)
+        if spec == "random":
+            self._check(lib().mrsim_set_policy_random(self._h))
+            return self
+        for prefix, greedy in (("feedforward:", True), ("feedforward_sample:", False)):
+            if spec.startswith(prefix):
+                path = spec[len(prefix):]
+                if not path:
+                    raise InvalidArgument("feedforward policy needs a weights file path")
+                return self.set_feedforward(FeedforwardWeights.load(path), greedy=greedy)
+        raise InvalidArgument(f"unknown policy '{spec}'")
+
+    def set_feedforward(self, weights: "FeedforwardWeights", greedy: bool = True):
+        dims, acts, flat = weights.packed()
+        self._check(lib().mrsim_set_policy_feedforward(
+            self._h, len(acts), dims.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+            acts.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), flat.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+            int(bool(greedy))))
+        return self
+
+    def policy_actions(self, stream=None):
+        """The context policy's actions for the current state (int8 cuda tensor [B, N])."""
+        self._check(lib().mrsim_policy_actions(self._h, ctypes.c_void_p(self._actions.data_ptr()),
+                                               _stream_handle(stream)))
+        return self._actions
+
     def sync(self, stream=None) -> None:
         self._check(lib().mrsim_sync(self._h, _stream_handle(stream)))
 
@@ -254,6 +285,97 @@ class CudaEnvBatch:
         s = _abi.Stats()
         self._check(lib().mrsim_get_stats(self._h, ctypes.byref(s)))
         return {f: getattr(s, f) for f, _ in _abi.Stats._fields_}
+
+
+class FeedforwardWeights:
+    """FeedforwardWeights (policy.hpp:69-195): dense layers (in, out, activation,
+    W out x in row-major, b). Text I/O follows the reference's self-describing
+    format (from_text / to_text, policy.hpp:134-195) so weight files written for
+    the reference load here unchanged."""
+
+    ACTIVATIONS = ("relu", "tanh", "identity")  # Activation order (policy.hpp:60)
+
+    def __init__(self, layers):
+        self.layers = [(int(i), int(o), str(a), np.asarray(w, dtype=np.float64).reshape(int(o), int(i)),
+                        np.asarray(b, dtype=np.float64).reshape(int(o))) for i, o, a, w, b in layers]
+        self.validate()
+
+    def validate(self) -> None:  # policy.hpp:77-93
+        if not self.layers:
+            raise InvalidArgument("weights: no layers")
+        for k, (i, o, a, w, b) in enumerate(self.layers):
+            if i <= 0 or o <= 0:
+                raise InvalidArgument("weights: bad layer dimensions")
+            if a not in self.ACTIVATIONS:
+                raise InvalidArgument(f"weights: unknown activation '{a}'")
+            if k > 0 and self.layers[k - 1][1] != i:
+                raise InvalidArgument("weights: layer dimensions do not chain")
+        if self.layers[-1][1] != 5:
+            raise InvalidArgument("weights: final layer must emit 5 logits")
+
+    @property
+    def input_dim(self) -> int:
+        return self.layers[0][0]
+
+    def packed(self):
+        dims = np.array([d for i, o, *_ in self.layers for d in (i, o)], dtype=np.int32)
+        acts = np.array([self.ACTIVATIONS.index(a) for _, _, a, _, _ in self.layers], dtype=np.int32)
+        flat = np.concatenate([np.concatenate([w.ravel(), b]) for *_, w, b in self.layers]).astype(np.float64)
+        return dims, acts, np.ascontiguousarray(flat)
+
+    @classmethod
+    def from_text(cls, text: str) -> "FeedforwardWeights":
+        tok = text.split()
+        pos = 0
+
+        def take():
+            nonlocal pos
+            if pos >= len(tok):
+                raise InvalidArgument("weights: truncated file")
+            pos += 1
+            return tok[pos - 1]
+
+        if take() != "mrsim-weights":
+            raise InvalidArgument("weights: missing 'mrsim-weights' magic")
+        if take() != "1":
+            raise InvalidArgument("weights: unsupported format version")
+        if take() != "layers":
+            raise InvalidArgument("weights: bad layer count")
+        n = int(take())
+        layers = []
+        for _ in range(n):
+            if take() != "layer":
+                raise InvalidArgument("weights: bad layer header")
+            take()  # index
+            i, o, a = int(take()), int(take()), take()
+            w = [float(take()) for _ in range(i * o)]
+            b = [float(take()) for _ in range(o)]
+            layers.append((i, o, a, w, b))
+        return cls(layers)
+
+    @classmethod
+    def load(cls, path: str) -> "FeedforwardWeights":
+        try:
+            with open(path) as f:
+                return cls.from_text(f.read())
+        except OSError:
+            raise RuntimeError(f"weights: cannot open '{path}'") from None
+
+    def to_text(self) -> str:
+        out = ["mrsim-weights 1", f"layers {len(self.layers)}"]
+        for k, (i, o, a, w, b) in enumerate(self.layers):
+            out.append(f"layer {k} {i} {o} {a}")
+            out += [" ".join(f"{v:.17g}" for v in row) for row in w]
+            out.append(" ".join(f"{v:.17g}" for v in b))
+        return "\n".join(out) + "\n"
+
+    @classmethod
+    def random(cls, dims, activations, seed: int = 0, scale: float = 1.0) -> "FeedforwardWeights":
+        rng = np.random.default_rng(seed)
+        layers = []
+        for (i, o), a in zip(zip(dims[:-1], dims[1:]), activations):
+            layers.append((i, o, a, rng.normal(0, scale / np.sqrt(i), (o, i)), rng.normal(0, 0.1, o)))
+        return cls(layers)
 
 
 def reset_batch(cfg: ScenarioConfig, seeds, device: int = 0, fp64: bool = True):

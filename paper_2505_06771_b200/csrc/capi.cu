@@ -51,6 +51,12 @@ struct mrsim_ctx {
     uint8_t* d_done = nullptr;
     int8_t* h_actions = nullptr;  // pinned
     bool reset_done = false;
+    // on-device feedforward policy (mrsim_set_policy_feedforward)
+    bool ff = false;
+    mrsim_dev::PolicyNet net{};
+    double* d_wT = nullptr;
+    double* d_bias = nullptr;
+    int8_t* d_pol_actions = nullptr;
 };
 
 namespace {
@@ -157,6 +163,40 @@ cudaError_t dispatch_reset(int task, const ResetParams<Real>& p, cudaStream_t s)
         case 7: return launch_reset<Real, 7>(p, s);
         default: return launch_reset<Real, 8>(p, s);
     }
+}
+
+template <class Real>
+cudaError_t dispatch_policy(int task, const mrsim_dev::PolicyParams<Real>& p, cudaStream_t s) {
+    using namespace mrsim_host;
+    switch (task) {
+        case 0: return launch_policy<Real, 0>(p, s);
+        case 1: return launch_policy<Real, 1>(p, s);
+        case 2: return launch_policy<Real, 2>(p, s);
+        case 3: return launch_policy<Real, 3>(p, s);
+        case 4: return launch_policy<Real, 4>(p, s);
+        case 5: return launch_policy<Real, 5>(p, s);
+        case 6: return launch_policy<Real, 6>(p, s);
+        case 7: return launch_policy<Real, 7>(p, s);
+        default: return launch_policy<Real, 8>(p, s);
+    }
+}
+
+template <class Real>
+cudaError_t policy_launch(mrsim_ctx* ctx, const DevState<Real>& st, int8_t* out, cudaStream_t s) {
+    mrsim_dev::PolicyParams<Real> p;
+    p.c = ctx->cfg;
+    p.s = st;
+    p.B = ctx->B;
+    p.N = ctx->N;
+    p.D = ctx->D;
+    p.bdim = ctx->bdim;
+    p.nf = ctx->nf;
+    p.ni = ctx->ni;
+    p.wT = ctx->d_wT;
+    p.bias = ctx->d_bias;
+    p.net = ctx->net;
+    p.actions = out;
+    return dispatch_policy<Real>(ctx->cfg.task, p, s);
 }
 
 template <class Real>
@@ -525,6 +565,14 @@ void from_host_states(mrsim_ctx* ctx, const DevState<Real>& s, long long first, 
     *err = e;
 }
 
+// The feedforward policy's actions for the current state (ctx->ff set).
+int run_policy(mrsim_ctx* ctx, int8_t* out, cudaStream_t s) {
+    const cudaError_t e = ctx->fp64 ? policy_launch<double>(ctx, ctx->sd[ctx->cur], out, s)
+                                    : policy_launch<float>(ctx, ctx->sf[ctx->cur], out, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "policy launch");
+    return MRSIM_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -630,6 +678,9 @@ void mrsim_destroy(mrsim_ctx* ctx) {
     cudaFree(ctx->d_reward64);
     cudaFree(ctx->d_done);
     if (ctx->h_actions) cudaFreeHost(ctx->h_actions);
+    cudaFree(ctx->d_wT);
+    cudaFree(ctx->d_bias);
+    cudaFree(ctx->d_pol_actions);
     delete ctx;
 }
 
@@ -676,6 +727,12 @@ int mrsim_step(mrsim_ctx* ctx, const int8_t* actions_dev, float* obs_dev, float*
     if ((ctx->flags & MRSIM_FLAG_AUTO_RESET) && !ctx->has_episodes)
         return set_err(ctx, MRSIM_E_INVALID_ARGUMENT, "auto-reset needs mrsim_reset_episodes (episode seeds)");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!actions_dev && ctx->ff) {  // the producer before the step: the feedforward policy on device
+        CK(cudaSetDevice(ctx->device));
+        const int rc = run_policy(ctx, ctx->d_pol_actions, s);
+        if (rc != MRSIM_OK) return rc;
+        actions_dev = ctx->d_pol_actions;
+    }
     return ctx->fp64 ? do_step<double>(ctx, ctx->sd, actions_dev, obs_dev, reward_dev, done_dev, next_obs_dev, s)
                      : do_step<float>(ctx, ctx->sf, actions_dev, obs_dev, reward_dev, done_dev, next_obs_dev, s);
 }
@@ -744,6 +801,79 @@ int mrsim_observe_host(mrsim_ctx* ctx, float* obs_host) {
     if (rc != MRSIM_OK) return rc;
     CK(cudaMemcpy(obs_host, ctx->d_obs, obs_bytes, cudaMemcpyDeviceToHost));
     return MRSIM_OK;
+}
+
+int mrsim_set_policy_random(mrsim_ctx* ctx) {
+    if (!ctx) return MRSIM_E_INVALID_ARGUMENT;
+    ctx->ff = false;
+    return MRSIM_OK;
+}
+
+int mrsim_set_policy_feedforward(mrsim_ctx* ctx, int num_layers, const int32_t* dims, const int32_t* activation,
+                                 const double* weights, int greedy) {
+    if (!ctx) return MRSIM_E_INVALID_ARGUMENT;
+    const int IA = MRSIM_E_INVALID_ARGUMENT;
+    // FeedforwardWeights::validate (policy.hpp:77-93)
+    if (num_layers <= 0 || !dims || !activation || !weights) return set_err(ctx, IA, "weights: no layers");
+    if (num_layers > MRSIM_POLICY_MAX_LAYERS)
+        return set_err(ctx, MRSIM_E_UNSUPPORTED, "device policy supports <= 8 layers");
+    mrsim_dev::PolicyNet net{};
+    net.num_layers = num_layers;
+    net.greedy = greedy ? 1 : 0;
+    long long wsz = 0, bsz = 0;
+    for (int l = 0; l < num_layers; ++l) {
+        const int in = dims[2 * l], out = dims[2 * l + 1];
+        if (in <= 0 || out <= 0) return set_err(ctx, IA, "weights: bad layer dimensions");
+        if (l > 0 && dims[2 * l - 1] != in) return set_err(ctx, IA, "weights: layer dimensions do not chain");
+        if (activation[l] < MRSIM_ACT_RELU || activation[l] > MRSIM_ACT_IDENTITY)
+            return set_err(ctx, IA, "weights: unknown activation");
+        if (in > MRSIM_POLICY_MAX_WIDTH || out > MRSIM_POLICY_MAX_WIDTH)
+            return set_err(ctx, MRSIM_E_UNSUPPORTED, "device policy supports layer widths <= 256");
+        net.in[l] = in;
+        net.out[l] = out;
+        net.act[l] = activation[l];
+        net.w_off[l] = wsz;
+        net.b_off[l] = bsz;
+        wsz += static_cast<long long>(in) * out;
+        bsz += out;
+    }
+    if (net.out[num_layers - 1] != 5) return set_err(ctx, IA, "weights: final layer must emit 5 logits");
+    if (net.in[0] != ctx->D)  // FeedforwardWeights::forward size check (policy.hpp:96-99)
+        return set_err(ctx, IA, "feedforward: observation size " + std::to_string(ctx->D) +
+                                    " does not match expected " + std::to_string(net.in[0]));
+    // transpose W (out x in) -> [in][out] per layer; split the biases out
+    std::vector<double> wT(static_cast<size_t>(wsz)), bias(static_cast<size_t>(bsz));
+    const double* src = weights;
+    for (int l = 0; l < num_layers; ++l) {
+        const int in = net.in[l], out = net.out[l];
+        for (int o = 0; o < out; ++o)
+            for (int i = 0; i < in; ++i) wT[net.w_off[l] + static_cast<long long>(i) * out + o] = src[o * in + i];
+        src += static_cast<long long>(in) * out;
+        for (int o = 0; o < out; ++o) bias[net.b_off[l] + o] = src[o];
+        src += out;
+    }
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaDeviceSynchronize());
+    cudaFree(ctx->d_wT);
+    cudaFree(ctx->d_bias);
+    ctx->d_wT = nullptr;
+    ctx->d_bias = nullptr;
+    ctx->ff = false;
+    CK(cudaMalloc(&ctx->d_wT, sizeof(double) * wT.size()));
+    CK(cudaMalloc(&ctx->d_bias, sizeof(double) * bias.size()));
+    CK(cudaMemcpy(ctx->d_wT, wT.data(), sizeof(double) * wT.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_bias, bias.data(), sizeof(double) * bias.size(), cudaMemcpyHostToDevice));
+    if (!ctx->d_pol_actions) CK(cudaMalloc(&ctx->d_pol_actions, ctx->B * ctx->N));
+    ctx->net = net;
+    ctx->ff = true;
+    return MRSIM_OK;
+}
+
+int mrsim_policy_actions(mrsim_ctx* ctx, int8_t* actions_dev, void* stream) {
+    if (!ctx || !actions_dev) return MRSIM_E_INVALID_ARGUMENT;
+    if (!ctx->ff) return mrsim_random_actions(ctx, actions_dev, stream);
+    CK(cudaSetDevice(ctx->device));
+    return run_policy(ctx, actions_dev, static_cast<cudaStream_t>(stream));
 }
 
 int mrsim_random_actions(mrsim_ctx* ctx, int8_t* actions_dev, void* stream) {

@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include "policy.cuh"
 #include "step_kernel.cuh"
 
 namespace mrsim_host {
@@ -68,5 +69,7 @@ cudaError_t launch_observe(const mrsim_cfg& c, const mrsim_dev::DevState<Real>& 
                            int bdim, int nf, int ni, cudaStream_t stream);
 template <class Real, int TASK>
 cudaError_t launch_reset(const mrsim_dev::ResetParams<Real>& p, cudaStream_t stream);
+template <class Real, int TASK>
+cudaError_t launch_policy(const mrsim_dev::PolicyParams<Real>& p, cudaStream_t stream);
 
 }  // namespace mrsim_host

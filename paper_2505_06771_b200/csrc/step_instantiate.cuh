@@ -111,4 +111,20 @@ cudaError_t launch_reset<double, MRSIM_TASK_ID>(const mrsim_dev::ResetParams<dou
     return cudaGetLastError();
 }
 
+template <class Real>
+static cudaError_t launch_policy_any(const mrsim_dev::PolicyParams<Real>& p, cudaStream_t s) {
+    const long long want = (p.B + mrsim_dev::kPolicyWarps - 1) / mrsim_dev::kPolicyWarps;
+    const unsigned grid = static_cast<unsigned>(want < 148 * 64 ? want : 148 * 64);
+    mrsim_dev::policy_kernel<Real, MRSIM_TASK_ID><<<grid, 32 * mrsim_dev::kPolicyWarps, 0, s>>>(p);
+    return cudaGetLastError();
+}
+template <>
+cudaError_t launch_policy<float, MRSIM_TASK_ID>(const mrsim_dev::PolicyParams<float>& p, cudaStream_t s) {
+    return launch_policy_any<float>(p, s);
+}
+template <>
+cudaError_t launch_policy<double, MRSIM_TASK_ID>(const mrsim_dev::PolicyParams<double>& p, cudaStream_t s) {
+    return launch_policy_any<double>(p, s);
+}
+
 }  // namespace mrsim_host

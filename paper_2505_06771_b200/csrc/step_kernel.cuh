@@ -711,7 +711,7 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
             float* o = p.obs + e * ND;
             for (int q = lane; q < ND; q += L) {
                 const int r = q / p.D;
-                o[q] = obs_feature<TASK, Real>(c, view, r, q - r * p.D, p.bdim);
+                o[q] = static_cast<float>(obs_feature<TASK, Real>(c, view, r, q - r * p.D, p.bdim));
             }
         }
 
@@ -753,7 +753,7 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
             float* o = p.next_obs + e * ND;
             for (int q = lane; q < ND; q += L) {
                 const int r = q / p.D;
-                o[q] = obs_feature<TASK, Real>(c, view, r, q - r * p.D, p.bdim);
+                o[q] = static_cast<float>(obs_feature<TASK, Real>(c, view, r, q - r * p.D, p.bdim));
             }
         }
 
@@ -838,7 +838,7 @@ __global__ void __launch_bounds__(128) reset_kernel(const __grid_constant__ Rese
         const EnvView<Real> v{xs, ys, ts, tf, ro.ti, N, drones, nullptr};
         float* o = p.obs + e * N * p.D;
         for (int r = 0; r < N; ++r)
-            for (int q = 0; q < p.D; ++q) o[r * p.D + q] = obs_feature<TASK, Real>(c, v, r, q, p.bdim);
+            for (int q = 0; q < p.D; ++q) o[r * p.D + q] = static_cast<float>(obs_feature<TASK, Real>(c, v, r, q, p.bdim));
     }
 }
 
@@ -862,7 +862,7 @@ __global__ void __launch_bounds__(128) observe_kernel(const __grid_constant__ mr
     const EnvView<Real> v{xs, ys, ts, tf, ti, N, drones, nullptr};
     float* o = obs + e * N * D;
     for (int r = 0; r < N; ++r)
-        for (int q = 0; q < D; ++q) o[r * D + q] = obs_feature<TASK, Real>(c, v, r, q, bdim);
+        for (int q = 0; q < D; ++q) o[r * D + q] = static_cast<float>(obs_feature<TASK, Real>(c, v, r, q, bdim));
 }
 
 // Harness random-policy actions for the current step of every env.

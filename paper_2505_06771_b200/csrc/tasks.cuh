@@ -575,74 +575,75 @@ __host__ __device__ inline int obs_dim_of(const mrsim_cfg& c) {
     return d;
 }
 
-// Feature q of robot r's observation: Scenario::observe + base_observation
+// Feature q of robot r's observation, in the state's precision (stores
+// round it to fp32; the on-device policy consumes it unrounded): Scenario::observe + base_observation
 // (scenario.hpp:200-210) + het_augment (framework.hpp:61-76).
 template <int TASK, class Real>
-__device__ float obs_feature(const mrsim_cfg& c, const EnvView<Real>& v, int r, int q, int bdim) {
+__device__ Real obs_feature(const mrsim_cfg& c, const EnvView<Real>& v, int r, int q, int bdim) {
     const int N = v.N;
     const mrsim_layout& L = c.layout;
     if (q >= bdim) {  // het_augment
         const int k = q - bdim;
-        if (c.het_obs_mode == MRSIM_HET_OBS_OWN) return static_cast<float>(c.het[r][k]);
-        return static_cast<float>(c.het[k / c.het_cols][k % c.het_cols]);
+        if (c.het_obs_mode == MRSIM_HET_OBS_OWN) return Real(c.het[r][k]);
+        return Real(c.het[k / c.het_cols][k % c.het_cols]);
     }
     if (TASK == MRSIM_TASK_RANDOM_WAYPOINTS) {  // random_waypoints.hpp:70-76: own pose + target
         switch (q) {
-            case 0: return static_cast<float>(v.xs[r]);
-            case 1: return static_cast<float>(v.ys[r]);
-            case 2: return static_cast<float>(v.ts[r]);
-            case 3: return static_cast<float>(v.tf[2 * r]);
-            default: return static_cast<float>(v.tf[2 * r + 1]);
+            case 0: return Real(v.xs[r]);
+            case 1: return Real(v.ys[r]);
+            case 2: return Real(v.ts[r]);
+            case 3: return Real(v.tf[2 * r]);
+            default: return Real(v.tf[2 * r + 1]);
         }
     }
     if (TASK == MRSIM_TASK_NAVIGATION) {  // navigation.hpp:96-102
         switch (q) {
-            case 0: return static_cast<float>(v.xs[r]);
-            case 1: return static_cast<float>(v.ys[r]);
-            case 2: return static_cast<float>(v.ts[r]);
-            case 3: return static_cast<float>(v.tf[2 * r] - v.xs[r]);
-            default: return static_cast<float>(v.tf[2 * r + 1] - v.ys[r]);
+            case 0: return Real(v.xs[r]);
+            case 1: return Real(v.ys[r]);
+            case 2: return Real(v.ts[r]);
+            case 3: return Real(v.tf[2 * r] - v.xs[r]);
+            default: return Real(v.tf[2 * r + 1] - v.ys[r]);
         }
     }
     const int base = 3 + 2 * (N - 1);
     if (q < base) {
-        if (q == 0) return static_cast<float>(v.xs[r]);
-        if (q == 1) return static_cast<float>(v.ys[r]);
-        if (q == 2) return static_cast<float>(v.ts[r]);
+        if (q == 0) return Real(v.xs[r]);
+        if (q == 1) return Real(v.ys[r]);
+        if (q == 2) return Real(v.ts[r]);
         const int k = (q - 3) >> 1;
         const int j = k < r ? k : k + 1;
-        return static_cast<float>(((q - 3) & 1) ? v.ys[j] : v.xs[j]);
+        return Real(((q - 3) & 1) ? v.ys[j] : v.xs[j]);
     }
     const int f = q - base;
-    if (TASK == MRSIM_TASK_PREDATOR_PREY) return static_cast<float>(v.tf[f]);
+    if (TASK == MRSIM_TASK_PREDATOR_PREY) return Real(v.tf[f]);
     if (TASK == MRSIM_TASK_DISCOVERY) {  // discovery.hpp:287-298
         const int k = f >> 1;
         const bool visible = ((v.ti[0] >> k) & 1) && !((v.ti[1] >> k) & 1);
-        return static_cast<float>(visible ? double(v.tf[f]) : L.discovery_sentinel[f & 1]);
+        return Real(visible ? double(v.tf[f]) : L.discovery_sentinel[f & 1]);
     }
     if (TASK == MRSIM_TASK_RWARE) {  // rware.hpp:111-124
         const int S = L.rware_num_slots;
         if (f < 3 * S) {
             const int sl = f / 3, comp = f % 3;
-            if (comp < 2) return static_cast<float>(L.rware_slots[2 * sl + comp]);
-            return static_cast<float>(ti_byte(v.ti, sl));
+            if (comp < 2) return Real(L.rware_slots[2 * sl + comp]);
+            return Real(ti_byte(v.ti, sl));
         }
         const int g2 = f - 3 * S;
-        if (g2 < rware_requests(L)) return static_cast<float>(ti_byte(v.ti, S + N + g2));
-        return static_cast<float>(ti_byte(v.ti, S + r));
+        if (g2 < rware_requests(L)) return Real(ti_byte(v.ti, S + N + g2));
+        return Real(ti_byte(v.ti, S + r));
     }
     if (TASK == MRSIM_TASK_FORAGING) {  // foraging.hpp:235-247
         const int rr = f / 3, comp = f % 3;
         const bool live = !((v.ti[0] >> rr) & 1);
-        if (comp < 2) return static_cast<float>(live ? double(v.tf[2 * rr + comp]) : L.discovery_sentinel[comp]);
-        return live ? static_cast<float>(v.ti[1 + rr]) : 0.0f;
+        if (comp < 2) return Real(live ? double(v.tf[2 * rr + comp]) : L.discovery_sentinel[comp]);
+        return live ? Real(v.ti[1 + rr]) : Real(0);
     }
     if (TASK == MRSIM_TASK_MATERIAL_TRANSPORT) {  // material_transport.hpp:77-85
-        if (f == 0) return static_cast<float>(v.tf[4 + r]);
-        return static_cast<float>(v.tf[f - 1]);  // 1 -> circle (tf[0]), 2 -> rect (tf[1])
+        if (f == 0) return Real(v.tf[4 + r]);
+        return Real(v.tf[f - 1]);  // 1 -> circle (tf[0]), 2 -> rect (tf[1])
     }
     if (TASK == MRSIM_TASK_ARCTIC_TRANSPORT) {  // arctic_transport.hpp:199-220
-        if (f == 0) return static_cast<float>(arctic_tile_at<Real>(c, v.ti, v.xs[r], v.ys[r]));
+        if (f == 0) return Real(arctic_tile_at<Real>(c, v.ti, v.xs[r], v.ys[r]));
         const int g2 = f - 1;
         const int which = g2 / 9, cell = g2 % 9;
         const int d = v.drones[which];  // which-th drone in robot-index order
@@ -654,10 +655,10 @@ __device__ float obs_feature(const mrsim_cfg& c, const EnvView<Real>& v, int r, 
         const int r0 = static_cast<int>(dclamp((v.ys[d] - (-hh)) / ch, Real(0), Real(rows - 1)));
         const int rr = r0 + cell / 3 - 1, cc = c0 + cell % 3 - 1;
         const bool in = rr >= 0 && rr < rows && cc >= 0 && cc < cols;
-        return in ? static_cast<float>(ti_byte(v.ti, rr * cols + cc)) : 0.0f;
+        return in ? Real(ti_byte(v.ti, rr * cols + cc)) : Real(0);
     }
     // warehouse.hpp:284-290
-    return ((v.ti[0] >> r) & 1) ? 1.0f : 0.0f;
+    return ((v.ti[0] >> r) & 1) ? Real(1) : Real(0);
 }
 
 }  // namespace mrsim_dev

@@ -39,6 +39,8 @@ def lib():
             "orc_step_env": (ctypes.c_int, [P(_abi.Cfg), P(_abi.EnvState), P(ctypes.c_int32), d, d, P(ctypes.c_int),
                                             ctypes.c_char_p, ctypes.c_int]),
             "orc_observe": (ctypes.c_int, [P(_abi.Cfg), P(_abi.EnvState), d]),
+            "orc_policy_act": (ctypes.c_int, [P(_abi.Cfg), P(_abi.EnvState), ctypes.c_int, ctypes.c_int,
+                                              P(ctypes.c_int32), P(ctypes.c_int32), d, ctypes.c_int]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -90,6 +92,13 @@ class OracleEnv:
         if rc:
             raise OracleError(rc, err.value.decode())
         return obs, rew.value, bool(done.value)
+
+
+def policy_act(cfg: _abi.Cfg, state: _abi.EnvState, robot: int, weights, greedy: bool = True) -> int:
+    dims, acts, flat = weights.packed()
+    return lib().orc_policy_act(ctypes.byref(cfg), ctypes.byref(state), robot, len(acts),
+                                dims.ctypes.data_as(P(ctypes.c_int32)), acts.ctypes.data_as(P(ctypes.c_int32)),
+                                dptr(flat), int(bool(greedy)))
 
 
 def solve_qp(A, b, lo, hi, u_nom, tol=1e-9, max_iter=0):

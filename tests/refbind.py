@@ -53,6 +53,8 @@ def lib():
                                               ctypes.c_int]),
             "ref_observe": (ctypes.c_int, [ctypes.c_void_p, P(ctypes.c_double)]),
             "ref_random_actions": (ctypes.c_int, [ctypes.c_void_p, P(ctypes.c_int32)]),
+            "ref_policy_actions": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, P(ctypes.c_int32),
+                                                  ctypes.c_char_p, ctypes.c_int]),
             "ref_time_steps": (ctypes.c_double, [ctypes.c_void_p, ctypes.c_int]),
             "ref_derive_episode_seed": (ctypes.c_uint64, [ctypes.c_uint64, ctypes.c_int]),
             "ref_policy_action": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_int, ctypes.c_int]),
@@ -178,6 +180,14 @@ class RefBatch:
     def random_actions(self):
         out = np.zeros((self.B, self.N), dtype=np.int32)
         lib().ref_random_actions(self.h, out.ctypes.data_as(P(ctypes.c_int32)))
+        return out
+
+    def policy_actions(self, spec: str):
+        out = np.zeros((self.B, self.N), dtype=np.int32)
+        err = ctypes.create_string_buffer(512)
+        rc = lib().ref_policy_actions(self.h, spec.encode(), out.ctypes.data_as(P(ctypes.c_int32)), err, 512)
+        if rc:
+            raise RefError(rc, err.value.decode())
         return out
 
     def time_steps(self, steps: int) -> float:

@@ -370,3 +370,45 @@ def test_barrier_on_rollouts_never_collide(name, orc):  # test_scenario_rules.cp
         assert env.state.min_pairwise_distance >= cfg.raw.safety_radius - 1e-3
         if done:
             env.reset(45 + t + 1)
+
+
+# ---- feedforward policy (policy.hpp:95-116, 445-480) ----
+
+@pytest.mark.parametrize("greedy", [True, False])
+@pytest.mark.parametrize("task,n", [("navigation", 4), ("discovery", 6), ("rware", 4), ("arctic_transport", 10)])
+def test_policy_actions_bit_exact_against_reference(task, n, greedy, orc, ref, tmp_path):
+    cfg, sp = cfg_and_spec(ref, task, n)
+    D = cfg.obs_dim
+    w = m.FeedforwardWeights.random([D, 32, 16, 5], ["relu", "tanh", "identity"], seed=n, scale=2.0)
+    path = tmp_path / "w.txt"
+    path.write_text(w.to_text())
+    spec = ("feedforward:" if greedy else "feedforward_sample:") + str(path)
+    rb = ref.RefBatch(sp)
+    seeds = [m.derive_episode_seed(9, e) for e in range(4)]
+    rb.reset(seeds)
+    envs = [orc.OracleEnv(cfg.raw) for _ in seeds]
+    for env, s in zip(envs, seeds):
+        env.reset(s)
+    for t in range(25):
+        ra = rb.policy_actions(spec)
+        for e, env in enumerate(envs):
+            oa = [orc.policy_act(cfg.raw, env.state, r, w, greedy) for r in range(n)]
+            assert oa == list(ra[e]), (t, e)
+        rb.step(ra)
+        for e, env in enumerate(envs):
+            env.step(ra[e])
+
+
+def test_weights_text_round_trip_and_errors(tmp_path):
+    w = m.FeedforwardWeights.random([5, 8, 5], ["tanh", "identity"], seed=3)
+    w2 = m.FeedforwardWeights.from_text(w.to_text())
+    for a, b in zip(w.layers, w2.layers):
+        assert a[:3] == b[:3] and np.array_equal(a[3], b[3]) and np.array_equal(a[4], b[4])
+    with pytest.raises(m.InvalidArgument, match="magic"):
+        m.FeedforwardWeights.from_text("nope 1")
+    with pytest.raises(m.InvalidArgument, match="5 logits"):
+        m.FeedforwardWeights.random([5, 4], ["identity"])
+    with pytest.raises(m.InvalidArgument, match="activation"):
+        m.FeedforwardWeights.random([5, 5], ["gelu"])
+    with pytest.raises(RuntimeError, match="cannot open"):
+        m.FeedforwardWeights.load(str(tmp_path / "missing.txt"))
