@@ -222,7 +222,7 @@ typedef struct mrsim_ctx mrsim_ctx;
 
 int mrsim_abi_version(void);
 /* sizeof of the ABI structs (0 mrsim_cfg, 1 mrsim_layout, 2 mrsim_env_state,
- * 3 mrsim_stats) so bindings can check their mirrors; -1 otherwise. */
+ * 3 mrsim_stats, 4 mrsim_traj_record) so bindings can check their mirrors; -1 otherwise. */
 int mrsim_sizeof(int which);
 /* make_default_config(name) (scenario.hpp:230-236) incl. configure_defaults of the task. */
 int mrsim_config_default(const char* scenario, mrsim_cfg* out);
@@ -232,6 +232,9 @@ int mrsim_config_default(const char* scenario, mrsim_cfg* out);
 int mrsim_config_set_num_robots(mrsim_cfg* cfg, int num_robots, int tile_roster);
 /* Layout::set (layout.hpp:130) for any key of the default table. */
 int mrsim_config_set_layout(mrsim_cfg* cfg, const char* key, const double* values, int count);
+/* Layout::get of a key (layout.hpp:98-105): writes up to max_count values,
+ * returns the value count, or -MRSIM_E_INVALID_ARGUMENT for an unknown key. */
+int mrsim_config_get_layout(const mrsim_cfg* cfg, const char* key, double* out, int max_count);
 /* ScenarioConfig::validate (framework.hpp:153-165) plus device-path limits. */
 int mrsim_config_validate(const mrsim_cfg* cfg, char* message, int message_len);
 /* Per-robot observation length after het_augment (batch.hpp:143-151). */
@@ -315,6 +318,36 @@ int mrsim_set_policy_random(mrsim_ctx* ctx);
 int mrsim_policy_actions(mrsim_ctx* ctx, int8_t* actions_dev, void* stream);
 /* Wait for the context's work on `stream` and report sticky device errors. */
 int mrsim_sync(mrsim_ctx* ctx, void* stream);
+
+/* ---- on-device trajectory capture (run_episodes rows, harness.hpp:257-286;
+ * TrajectoryRow, trajectory.hpp:38-82) ---- */
+typedef struct mrsim_traj_record {
+    double x, y, theta;             /* robot pose after the step */
+    double reward;                  /* team reward of the step (StepOutput::team_reward) */
+    double metric;                  /* Metrics::scenario_metric snapshot */
+    int64_t collisions;             /* Metrics::collisions, cumulative within the episode */
+    int32_t action;                 /* the action the robot took */
+    int32_t done;                   /* StepOutput::done */
+} mrsim_traj_record;
+/* Start recording every subsequent mrsim_step (up to max_steps steps) into a
+ * device buffer [max_steps][num_envs][N]; with actions_dev = NULL the policy's
+ * actions are materialised so they can be recorded. Not allowed with
+ * MRSIM_FLAG_AUTO_RESET (run_episodes waves do not auto-reset). Synchronous. */
+int mrsim_capture_begin(mrsim_ctx* ctx, int64_t max_steps);
+/* Steps recorded so far. */
+int64_t mrsim_capture_steps(const mrsim_ctx* ctx);
+/* Copy the records of envs [first_env, first_env+count) to host, laid out
+ * [steps][count][N]. Synchronous. */
+int mrsim_capture_read(mrsim_ctx* ctx, int64_t first_env, int64_t count, mrsim_traj_record* out);
+/* Stop recording and free the buffer. */
+int mrsim_capture_end(mrsim_ctx* ctx);
+/* Host-side writer of the trajectory data section (write_trajectory,
+ * trajectory.hpp:116-134): header_text (magic, config-hash, fields, column
+ * line; built by the caller) verbatim, then one CSV row per (env, step,
+ * robot), env-major, floats as %.17g. recs: [steps][envs][N]; rows carry env
+ * index env_offset + e. append != 0 appends rows only (later waves). */
+int mrsim_trajectory_write(const char* path, const char* header_text, const mrsim_traj_record* recs,
+                           int64_t steps, int64_t envs, int num_robots, int64_t env_offset, int append);
 
 /* Download / upload EnvState records of envs [first, first+count). Synchronous. */
 int mrsim_get_env_states(mrsim_ctx* ctx, int64_t first, int64_t count, mrsim_env_state* out);

@@ -728,6 +728,65 @@ int ref_apply_barrier(void* h, int n, const double* poses, const double* nominal
     }
 }
 
+// run_episodes (harness.hpp:216-300) writing the reference trajectory file
+// (trajectory.hpp:116-134) for the given policy / controller / layout.
+int ref_run_episodes_file(const char* scenario, std::uint64_t seed, int episodes, int batch, int num_robots,
+                          int max_steps, const char* policy, const char* controller, const char* layout,
+                          const char* out_path, char* err, int errlen) {
+    try {
+        RunConfig run;
+        run.scenario = scenario;
+        run.seed = seed;
+        run.episodes = episodes;
+        run.batch = batch;
+        run.workers = 1;
+        run.num_robots = num_robots;
+        run.max_steps = max_steps;
+        run.policy = policy;
+        run.controller = controller ? controller : "";
+        run.out = out_path;
+        if (layout && *layout) {
+            std::istringstream all(layout);
+            std::string item;
+            while (std::getline(all, item, ';')) {
+                std::istringstream is(item);
+                std::string key;
+                is >> key;
+                std::vector<double> vals;
+                double v;
+                while (is >> v) vals.push_back(v);
+                if (!key.empty()) run.layout_overrides[key] = vals;
+            }
+        }
+        run_episodes(run, true);
+        return 0;
+    } catch (const std::exception& e) {
+        put_err(err, errlen, e);
+        return code_of(e);
+    }
+}
+
+// verify_trajectory (harness.hpp:444-518): 1 ok, 0 diverged (msg set).
+int ref_verify_trajectory(const char* path, char* msg, int len, long long* first_row) {
+    VerifyReport r = verify_trajectory(path);
+    if (msg && len > 0) {
+        std::strncpy(msg, r.message.c_str(), static_cast<std::size_t>(len) - 1);
+        msg[len - 1] = 0;
+    }
+    if (first_row) *first_row = r.first_divergent_row;
+    return r.ok ? 1 : 0;
+}
+
+// read_trajectory (trajectory.hpp:136-180): row count, or -code on a format error.
+long ref_read_trajectory(const char* path, char* err, int errlen) {
+    try {
+        return static_cast<long>(read_trajectory(std::string(path)).rows.size());
+    } catch (const std::exception& e) {
+        put_err(err, errlen, e);
+        return -code_of(e);
+    }
+}
+
 // run_episodes (harness.hpp:216-300) with the random policy, no file written.
 // rows_out: [episodes*max_steps*N][11] = env, step, robot, x, y, theta, action,
 // reward, done, collisions, metric. Returns the row count or -code.

@@ -75,6 +75,7 @@ Layout = STRUCTS["mrsim_layout"]
 Cfg = STRUCTS["mrsim_cfg"]
 EnvState = STRUCTS["mrsim_env_state"]
 Stats = STRUCTS["mrsim_stats"]
+TrajRecord = STRUCTS["mrsim_traj_record"]
 globals().update(DEFINES)
 
 # Every function the header declares (name -> (restype, argtypes)).
@@ -86,6 +87,7 @@ FUNCTIONS = {
     "mrsim_config_default": (ctypes.c_int, [ctypes.c_char_p, P(Cfg)]),
     "mrsim_config_set_num_robots": (ctypes.c_int, [P(Cfg), ctypes.c_int, ctypes.c_int]),
     "mrsim_config_set_layout": (ctypes.c_int, [P(Cfg), ctypes.c_char_p, P(ctypes.c_double), ctypes.c_int]),
+    "mrsim_config_get_layout": (ctypes.c_int, [P(Cfg), ctypes.c_char_p, P(ctypes.c_double), ctypes.c_int]),
     "mrsim_config_validate": (ctypes.c_int, [P(Cfg), ctypes.c_char_p, ctypes.c_int]),
     "mrsim_obs_dim": (ctypes.c_int, [P(Cfg)]),
     "mrsim_task_name": (ctypes.c_char_p, [ctypes.c_int]),
@@ -108,6 +110,12 @@ FUNCTIONS = {
     "mrsim_set_policy_random": (ctypes.c_int, [c_void_p]),
     "mrsim_policy_actions": (ctypes.c_int, [c_void_p, c_void_p, c_void_p]),
     "mrsim_sync": (ctypes.c_int, [c_void_p, c_void_p]),
+    "mrsim_capture_begin": (ctypes.c_int, [c_void_p, ctypes.c_int64]),
+    "mrsim_capture_steps": (ctypes.c_int64, [c_void_p]),
+    "mrsim_capture_read": (ctypes.c_int, [c_void_p, ctypes.c_int64, ctypes.c_int64, c_void_p]),
+    "mrsim_capture_end": (ctypes.c_int, [c_void_p]),
+    "mrsim_trajectory_write": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, c_void_p, ctypes.c_int64,
+                                              ctypes.c_int64, ctypes.c_int, ctypes.c_int64, ctypes.c_int]),
     "mrsim_get_env_states": (ctypes.c_int, [c_void_p, ctypes.c_int64, ctypes.c_int64, P(EnvState)]),
     "mrsim_set_env_states": (ctypes.c_int, [c_void_p, ctypes.c_int64, ctypes.c_int64, P(EnvState)]),
     "mrsim_get_stats": (ctypes.c_int, [c_void_p, P(Stats)]),

@@ -64,7 +64,7 @@ def lib() -> ctypes.CDLL:
             fn.argtypes = args
         if handle.mrsim_abi_version() != _abi.MRSIM_ABI_VERSION:
             raise ImportError("libmrsim_cuda.so ABI version does not match include/mrsim_cuda.h")
-        for which, st in enumerate((_abi.Cfg, _abi.Layout, _abi.EnvState, _abi.Stats)):
+        for which, st in enumerate((_abi.Cfg, _abi.Layout, _abi.EnvState, _abi.Stats, _abi.TrajRecord)):
             if handle.mrsim_sizeof(which) != ctypes.sizeof(st):
                 raise ImportError(f"ctypes mirror of {st.__name__} has the wrong size")
         _lib = handle

@@ -91,6 +91,13 @@ class ScenarioConfig:
         raise_for(rc, f"layout: bad key or value count for '{key}'")
         return self
 
+    def get_layout(self, key: str) -> list:
+        buf = (ctypes.c_double * 64)()
+        n = lib().mrsim_config_get_layout(ctypes.byref(self.raw), key.encode(), buf, 64)
+        if n < 0:
+            raise InvalidArgument(f"layout: unknown key '{key}'")
+        return list(buf[:n])
+
     def validate(self) -> None:
         buf = ctypes.create_string_buffer(256)
         rc = lib().mrsim_config_validate(ctypes.byref(self.raw), buf, 256)

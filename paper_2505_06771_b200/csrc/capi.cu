@@ -57,6 +57,9 @@ struct mrsim_ctx {
     double* d_wT = nullptr;
     double* d_bias = nullptr;
     int8_t* d_pol_actions = nullptr;
+    // trajectory capture (mrsim_capture_begin)
+    mrsim_traj_record* d_cap = nullptr;
+    long long cap_max = 0, cap_steps = 0;
 };
 
 namespace {
@@ -573,6 +576,52 @@ int run_policy(mrsim_ctx* ctx, int8_t* out, cudaStream_t s) {
     return MRSIM_OK;
 }
 
+
+template <class Real>
+cudaError_t capture_launch(mrsim_ctx* ctx, const DevState<Real>& st, const int8_t* actions, const uint8_t* done,
+                           cudaStream_t s) {
+    const long long total = ctx->B * ctx->N;
+    const unsigned grid = static_cast<unsigned>((total + 255) / 256);
+    mrsim_dev::capture_kernel<Real><<<grid, 256, 0, s>>>(st, actions, ctx->d_reward64, done, ctx->B, ctx->N,
+                                                         ctx->d_cap + ctx->cap_steps * total);
+    return cudaGetLastError();
+}
+
+// A step while capturing: materialise the policy's actions (when not given),
+// step with a double team reward, then record (env, robot) rows of the new state.
+int capture_step(mrsim_ctx* ctx, const int8_t* actions, float* obs, float* reward, uint8_t* done, float* next_obs,
+                 cudaStream_t s) {
+    if (ctx->cap_steps >= ctx->cap_max) return set_err(ctx, MRSIM_E_INVALID_ARGUMENT, "trajectory capture buffer full");
+    CK(cudaSetDevice(ctx->device));
+    const long long BN = ctx->B * ctx->N;
+    if (!ctx->d_reward64) CK(cudaMalloc(&ctx->d_reward64, 8 * ctx->B));
+    if (!ctx->d_done) CK(cudaMalloc(&ctx->d_done, ctx->B));
+    if (!actions) {
+        if (!ctx->d_pol_actions) CK(cudaMalloc(&ctx->d_pol_actions, BN));
+        int rc = ctx->ff ? run_policy(ctx, ctx->d_pol_actions, s) : MRSIM_OK;
+        if (!ctx->ff) {
+            const unsigned grid = static_cast<unsigned>((BN + 255) / 256);
+            if (ctx->fp64)
+                mrsim_dev::random_actions_kernel<double><<<grid, 256, 0, s>>>(
+                    ctx->sd[ctx->cur].step_index, ctx->sd[ctx->cur].pkey, ctx->N, ctx->B, ctx->d_pol_actions);
+            else
+                mrsim_dev::random_actions_kernel<float><<<grid, 256, 0, s>>>(
+                    ctx->sf[ctx->cur].step_index, ctx->sf[ctx->cur].pkey, ctx->N, ctx->B, ctx->d_pol_actions);
+            CK(cudaGetLastError());
+        }
+        if (rc != MRSIM_OK) return rc;
+        actions = ctx->d_pol_actions;
+    }
+    uint8_t* dn = done ? done : ctx->d_done;
+    int rc = ctx->fp64 ? do_step<double>(ctx, ctx->sd, actions, obs, reward, dn, next_obs, s, ctx->d_reward64)
+                       : do_step<float>(ctx, ctx->sf, actions, obs, reward, dn, next_obs, s, ctx->d_reward64);
+    if (rc != MRSIM_OK) return rc;
+    const cudaError_t e = ctx->fp64 ? capture_launch<double>(ctx, ctx->sd[ctx->cur], actions, dn, s)
+                                    : capture_launch<float>(ctx, ctx->sf[ctx->cur], actions, dn, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "capture launch");
+    ctx->cap_steps += 1;
+    return MRSIM_OK;
+}
 }  // namespace
 
 extern "C" {
@@ -681,6 +730,7 @@ void mrsim_destroy(mrsim_ctx* ctx) {
     cudaFree(ctx->d_wT);
     cudaFree(ctx->d_bias);
     cudaFree(ctx->d_pol_actions);
+    cudaFree(ctx->d_cap);
     delete ctx;
 }
 
@@ -727,6 +777,7 @@ int mrsim_step(mrsim_ctx* ctx, const int8_t* actions_dev, float* obs_dev, float*
     if ((ctx->flags & MRSIM_FLAG_AUTO_RESET) && !ctx->has_episodes)
         return set_err(ctx, MRSIM_E_INVALID_ARGUMENT, "auto-reset needs mrsim_reset_episodes (episode seeds)");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (ctx->d_cap) return capture_step(ctx, actions_dev, obs_dev, reward_dev, done_dev, next_obs_dev, s);
     if (!actions_dev && ctx->ff) {  // the producer before the step: the feedforward policy on device
         CK(cudaSetDevice(ctx->device));
         const int rc = run_policy(ctx, ctx->d_pol_actions, s);
@@ -890,6 +941,44 @@ int mrsim_random_actions(mrsim_ctx* ctx, int8_t* actions_dev, void* stream) {
         mrsim_dev::random_actions_kernel<float><<<grid, block, 0, s>>>(
             ctx->sf[ctx->cur].step_index, ctx->sf[ctx->cur].pkey, ctx->N, ctx->B, actions_dev);
     CK(cudaGetLastError());
+    return MRSIM_OK;
+}
+
+int mrsim_capture_begin(mrsim_ctx* ctx, int64_t max_steps) {
+    if (!ctx || max_steps < 1) return MRSIM_E_INVALID_ARGUMENT;
+    if (ctx->flags & MRSIM_FLAG_AUTO_RESET)
+        return set_err(ctx, MRSIM_E_INVALID_ARGUMENT, "trajectory capture needs a context without auto-reset");
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaDeviceSynchronize());
+    cudaFree(ctx->d_cap);
+    ctx->d_cap = nullptr;
+    ctx->cap_max = ctx->cap_steps = 0;
+    CK(cudaMalloc(&ctx->d_cap, sizeof(mrsim_traj_record) * max_steps * ctx->B * ctx->N));
+    ctx->cap_max = max_steps;
+    return MRSIM_OK;
+}
+
+int64_t mrsim_capture_steps(const mrsim_ctx* ctx) { return ctx ? ctx->cap_steps : 0; }
+
+int mrsim_capture_read(mrsim_ctx* ctx, int64_t first_env, int64_t count, mrsim_traj_record* out) {
+    if (!ctx || !out || !ctx->d_cap || first_env < 0 || count < 0 || first_env + count > ctx->B)
+        return MRSIM_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaDeviceSynchronize());
+    const size_t rec = sizeof(mrsim_traj_record);
+    const size_t width = rec * count * ctx->N, pitch = rec * ctx->B * ctx->N;
+    CK(cudaMemcpy2D(out, width, ctx->d_cap + first_env * ctx->N, pitch, width, ctx->cap_steps,
+                    cudaMemcpyDeviceToHost));
+    return check_device_error(ctx, true);
+}
+
+int mrsim_capture_end(mrsim_ctx* ctx) {
+    if (!ctx) return MRSIM_E_INVALID_ARGUMENT;
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaDeviceSynchronize());
+    cudaFree(ctx->d_cap);
+    ctx->d_cap = nullptr;
+    ctx->cap_max = ctx->cap_steps = 0;
     return MRSIM_OK;
 }
 

@@ -120,6 +120,69 @@ uint32_t required_coefs(int task) {
 
 }  // namespace
 
+namespace {
+struct LayoutEnt {
+    const char* key;
+    double* d;
+    int32_t* i;
+    int arity;
+};
+// Layout keys (layout.hpp:28-87) -> fields of mrsim_layout; false if unknown.
+bool layout_entry(mrsim_layout& y, const char* key, LayoutEnt* out) {
+    const LayoutEnt table[] = {
+
+        {"spawn.margin", &y.spawn_margin, nullptr, 1},
+        {"spawn.separation_slack", &y.spawn_separation_slack, nullptr, 1},
+        {"arctic.grid_cols", nullptr, &y.arctic_grid_cols, 1},
+        {"arctic.grid_rows", nullptr, &y.arctic_grid_rows, 1},
+        {"arctic.ground_cols_left", nullptr, &y.arctic_ground_cols_left, 1},
+        {"arctic.ground_cols_right", nullptr, &y.arctic_ground_cols_right, 1},
+        {"arctic.goal_zone", y.arctic_goal_zone, nullptr, 4},
+        {"arctic.spawn_zone", y.arctic_spawn_zone, nullptr, 4},
+        {"arctic.normal_step", &y.arctic_normal_step, nullptr, 1},
+        {"arctic.fast_step", &y.arctic_fast_step, nullptr, 1},
+        {"arctic.slow_step", &y.arctic_slow_step, nullptr, 1},
+        {"discovery.num_landmarks", nullptr, &y.discovery_num_landmarks, 1},
+        {"discovery.landmark_margin", &y.discovery_landmark_margin, nullptr, 1},
+        {"discovery.sentinel", y.discovery_sentinel, nullptr, 2},
+        {"foraging.num_resources", nullptr, &y.foraging_num_resources, 1},
+        {"foraging.radius", &y.foraging_radius, nullptr, 1},
+        {"foraging.resource_margin", &y.foraging_resource_margin, nullptr, 1},
+        {"mt.circle_zone", y.mt_circle_zone, nullptr, 3},
+        {"mt.rect_zone", y.mt_rect_zone, nullptr, 4},
+        {"mt.dropoff_zone", y.mt_dropoff_zone, nullptr, 4},
+        {"mt.circle_mean", &y.mt_circle_mean, nullptr, 1},
+        {"mt.circle_variance", &y.mt_circle_variance, nullptr, 1},
+        {"mt.rect_mean", &y.mt_rect_mean, nullptr, 1},
+        {"mt.rect_variance", &y.mt_rect_variance, nullptr, 1},
+        {"navigation.goal_margin", &y.navigation_goal_margin, nullptr, 1},
+        {"navigation.goal_separation", &y.navigation_goal_separation, nullptr, 1},
+        {"navigation.on_goal_radius", &y.navigation_on_goal_radius, nullptr, 1},
+        {"pp.tag_radius", &y.pp_tag_radius, nullptr, 1},
+        {"pp.prey_agility", &y.pp_prey_agility, nullptr, 1},
+        {"pp.prey_spawn_clearance", &y.pp_prey_spawn_clearance, nullptr, 1},
+        {"pp.flash_steps", nullptr, &y.pp_flash_steps, 1},
+        {"rware.slot_half", &y.rware_slot_half, nullptr, 1},
+        {"rware.shelf_radius", &y.rware_shelf_radius, nullptr, 1},
+        {"rware.num_shelves", nullptr, &y.rware_num_shelves, 1},
+        {"rware.request_size", nullptr, &y.rware_request_size, 1},
+        {"rware.dropoff_zone", y.rware_dropoff_zone, nullptr, 4},
+        {"warehouse.green_right", y.warehouse_green_right, nullptr, 4},
+        {"warehouse.red_right", y.warehouse_red_right, nullptr, 4},
+        {"warehouse.green_left", y.warehouse_green_left, nullptr, 4},
+        {"warehouse.red_left", y.warehouse_red_left, nullptr, 4},
+        {"rwp.waypoint_margin", &y.rwp_waypoint_margin, nullptr, 1},
+        {"rwp.arrival_tolerance", &y.rwp_arrival_tolerance, nullptr, 1},
+    };
+    for (const LayoutEnt& e : table)
+        if (std::strcmp(key, e.key) == 0) {
+            *out = e;
+            return true;
+        }
+    return false;
+}
+}  // namespace
+
 extern "C" {
 
 int mrsim_abi_version(void) { return MRSIM_ABI_VERSION; }
@@ -130,6 +193,7 @@ int mrsim_sizeof(int which) {
         case 1: return static_cast<int>(sizeof(mrsim_layout));
         case 2: return static_cast<int>(sizeof(mrsim_env_state));
         case 3: return static_cast<int>(sizeof(mrsim_stats));
+        case 4: return static_cast<int>(sizeof(mrsim_traj_record));
         default: return -1;
     }
 }
@@ -265,55 +329,6 @@ int mrsim_config_set_num_robots(mrsim_cfg* c, int n, int tile_roster) {
 int mrsim_config_set_layout(mrsim_cfg* c, const char* key, const double* v, int count) {
     if (!c || !key || (count > 0 && !v)) return MRSIM_E_INVALID_ARGUMENT;
     mrsim_layout& y = c->layout;
-    struct Ent {
-        const char* key;
-        double* d;
-        int32_t* i;
-        int arity;
-    } table[] = {
-        {"spawn.margin", &y.spawn_margin, nullptr, 1},
-        {"spawn.separation_slack", &y.spawn_separation_slack, nullptr, 1},
-        {"arctic.grid_cols", nullptr, &y.arctic_grid_cols, 1},
-        {"arctic.grid_rows", nullptr, &y.arctic_grid_rows, 1},
-        {"arctic.ground_cols_left", nullptr, &y.arctic_ground_cols_left, 1},
-        {"arctic.ground_cols_right", nullptr, &y.arctic_ground_cols_right, 1},
-        {"arctic.goal_zone", y.arctic_goal_zone, nullptr, 4},
-        {"arctic.spawn_zone", y.arctic_spawn_zone, nullptr, 4},
-        {"arctic.normal_step", &y.arctic_normal_step, nullptr, 1},
-        {"arctic.fast_step", &y.arctic_fast_step, nullptr, 1},
-        {"arctic.slow_step", &y.arctic_slow_step, nullptr, 1},
-        {"discovery.num_landmarks", nullptr, &y.discovery_num_landmarks, 1},
-        {"discovery.landmark_margin", &y.discovery_landmark_margin, nullptr, 1},
-        {"discovery.sentinel", y.discovery_sentinel, nullptr, 2},
-        {"foraging.num_resources", nullptr, &y.foraging_num_resources, 1},
-        {"foraging.radius", &y.foraging_radius, nullptr, 1},
-        {"foraging.resource_margin", &y.foraging_resource_margin, nullptr, 1},
-        {"mt.circle_zone", y.mt_circle_zone, nullptr, 3},
-        {"mt.rect_zone", y.mt_rect_zone, nullptr, 4},
-        {"mt.dropoff_zone", y.mt_dropoff_zone, nullptr, 4},
-        {"mt.circle_mean", &y.mt_circle_mean, nullptr, 1},
-        {"mt.circle_variance", &y.mt_circle_variance, nullptr, 1},
-        {"mt.rect_mean", &y.mt_rect_mean, nullptr, 1},
-        {"mt.rect_variance", &y.mt_rect_variance, nullptr, 1},
-        {"navigation.goal_margin", &y.navigation_goal_margin, nullptr, 1},
-        {"navigation.goal_separation", &y.navigation_goal_separation, nullptr, 1},
-        {"navigation.on_goal_radius", &y.navigation_on_goal_radius, nullptr, 1},
-        {"pp.tag_radius", &y.pp_tag_radius, nullptr, 1},
-        {"pp.prey_agility", &y.pp_prey_agility, nullptr, 1},
-        {"pp.prey_spawn_clearance", &y.pp_prey_spawn_clearance, nullptr, 1},
-        {"pp.flash_steps", nullptr, &y.pp_flash_steps, 1},
-        {"rware.slot_half", &y.rware_slot_half, nullptr, 1},
-        {"rware.shelf_radius", &y.rware_shelf_radius, nullptr, 1},
-        {"rware.num_shelves", nullptr, &y.rware_num_shelves, 1},
-        {"rware.request_size", nullptr, &y.rware_request_size, 1},
-        {"rware.dropoff_zone", y.rware_dropoff_zone, nullptr, 4},
-        {"warehouse.green_right", y.warehouse_green_right, nullptr, 4},
-        {"warehouse.red_right", y.warehouse_red_right, nullptr, 4},
-        {"warehouse.green_left", y.warehouse_green_left, nullptr, 4},
-        {"warehouse.red_left", y.warehouse_red_left, nullptr, 4},
-        {"rwp.waypoint_margin", &y.rwp_waypoint_margin, nullptr, 1},
-        {"rwp.arrival_tolerance", &y.rwp_arrival_tolerance, nullptr, 1},
-    };
     if (std::strcmp(key, "rware.slots") == 0) {  // point list (layout.hpp:121-128)
         if (count % 2 != 0) return MRSIM_E_INVALID_ARGUMENT;
         if (count / 2 > MRSIM_MAX_SLOTS) return MRSIM_E_UNSUPPORTED;
@@ -321,16 +336,28 @@ int mrsim_config_set_layout(mrsim_cfg* c, const char* key, const double* v, int 
         for (int i = 0; i < 2 * MRSIM_MAX_SLOTS; ++i) y.rware_slots[i] = i < count ? v[i] : 0.0;
         return MRSIM_OK;
     }
-    for (const Ent& e : table) {
-        if (std::strcmp(key, e.key) != 0) continue;
-        if (count != e.arity) return MRSIM_E_INVALID_ARGUMENT;
-        for (int k = 0; k < count; ++k) {
-            if (e.d) e.d[k] = v[k];
-            else e.i[k] = static_cast<int32_t>(v[k]);  // Layout::integer (layout.hpp:105)
-        }
-        return MRSIM_OK;
+    LayoutEnt e;
+    if (!layout_entry(y, key, &e)) return MRSIM_E_INVALID_ARGUMENT;  // unknown key
+    if (count != e.arity) return MRSIM_E_INVALID_ARGUMENT;
+    for (int k = 0; k < count; ++k) {
+        if (e.d) e.d[k] = v[k];
+        else e.i[k] = static_cast<int32_t>(v[k]);  // Layout::integer (layout.hpp:105)
     }
-    return MRSIM_E_INVALID_ARGUMENT;  // unknown key
+    return MRSIM_OK;
+}
+
+int mrsim_config_get_layout(const mrsim_cfg* c, const char* key, double* out, int max_count) {
+    if (!c || !key || !out) return -MRSIM_E_INVALID_ARGUMENT;
+    mrsim_layout y = c->layout;
+    if (std::strcmp(key, "rware.slots") == 0) {
+        const int n = 2 * y.rware_num_slots;
+        for (int k = 0; k < n && k < max_count; ++k) out[k] = y.rware_slots[k];
+        return n;
+    }
+    LayoutEnt e;
+    if (!layout_entry(y, key, &e)) return -MRSIM_E_INVALID_ARGUMENT;
+    for (int k = 0; k < e.arity && k < max_count; ++k) out[k] = e.d ? e.d[k] : static_cast<double>(e.i[k]);
+    return e.arity;
 }
 
 int mrsim_config_validate(const mrsim_cfg* cp, char* msg, int len) {

@@ -876,4 +876,23 @@ __global__ void random_actions_kernel(const int32_t* step_index, const uint64_t*
     out[t] = static_cast<int8_t>(policy_action(pkey[e], step_index[e], r));
 }
 
+// One trajectory record per (env, robot) of the state a step just wrote.
+template <class Real>
+__global__ void capture_kernel(DevState<Real> s, const int8_t* actions, const double* reward64, const uint8_t* done,
+                               long long B, int N, mrsim_traj_record* out) {
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= B * N) return;
+    const long long e = t / N;
+    mrsim_traj_record rec;
+    rec.x = double(s.px[t]);
+    rec.y = double(s.py[t]);
+    rec.theta = double(s.pt[t]);
+    rec.reward = reward64[e];
+    rec.metric = double(s.metric[e]);
+    rec.collisions = s.collisions[e];
+    rec.action = actions[t];
+    rec.done = done[e];
+    out[t] = rec;
+}
+
 }  // namespace mrsim_dev

@@ -53,6 +53,13 @@ def lib():
                                               ctypes.c_int]),
             "ref_observe": (ctypes.c_int, [ctypes.c_void_p, P(ctypes.c_double)]),
             "ref_random_actions": (ctypes.c_int, [ctypes.c_void_p, P(ctypes.c_int32)]),
+            "ref_run_episodes_file": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
+                                                     ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.c_char_p,
+                                                     ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p,
+                                                     ctypes.c_int]),
+            "ref_verify_trajectory": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int,
+                                                     P(ctypes.c_longlong)]),
+            "ref_read_trajectory": (ctypes.c_long, [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int]),
             "ref_policy_actions": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, P(ctypes.c_int32),
                                                   ctypes.c_char_p, ctypes.c_int]),
             "ref_time_steps": (ctypes.c_double, [ctypes.c_void_p, ctypes.c_int]),
@@ -258,3 +265,29 @@ def run_episodes(scenario: str, seed: int, episodes: int, batch: int, max_steps:
     if k < 0:
         raise RefError(-k, err.value.decode())
     return rows[:k]
+
+
+def run_episodes_file(path: str, scenario: str, seed: int, episodes: int, batch: int, num_robots: int = -1,
+                      max_steps: int = -1, policy: str = "random", controller: str = "",
+                      layout: dict | None = None) -> None:
+    text = ";".join(f"{k} " + " ".join(repr(float(v)) for v in vals) for k, vals in (layout or {}).items())
+    err = ctypes.create_string_buffer(512)
+    rc = lib().ref_run_episodes_file(scenario.encode(), seed, episodes, batch, num_robots, max_steps,
+                                     policy.encode(), controller.encode(), text.encode(), path.encode(), err, 512)
+    if rc:
+        raise RefError(rc, err.value.decode())
+
+
+def verify_trajectory(path: str):
+    msg = ctypes.create_string_buffer(2048)
+    row = ctypes.c_longlong()
+    ok = lib().ref_verify_trajectory(path.encode(), msg, 2048, ctypes.byref(row))
+    return bool(ok), msg.value.decode(), row.value
+
+
+def read_trajectory_rows(path: str) -> int:
+    err = ctypes.create_string_buffer(512)
+    k = lib().ref_read_trajectory(path.encode(), err, 512)
+    if k < 0:
+        raise RefError(-k, err.value.decode())
+    return k

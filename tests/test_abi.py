@@ -25,7 +25,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_struct_sizes_match_header_mirror():
     lib = m.lib()
-    for which, st in enumerate((_abi.Cfg, _abi.Layout, _abi.EnvState, _abi.Stats)):
+    for which, st in enumerate((_abi.Cfg, _abi.Layout, _abi.EnvState, _abi.Stats, _abi.TrajRecord)):
         assert lib.mrsim_sizeof(which) == ctypes.sizeof(st)
     assert lib.mrsim_sizeof(9) == -1
 
