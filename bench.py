@@ -248,23 +248,28 @@ def main():
     e2e = None
     if a.e2e_steps > 0:
         rng = np.random.default_rng(rank)
-        acts = rng.integers(0, 5, size=(a.e2e_steps, B, a.robots), dtype=np.int32)
+        # pinned host buffers: the step's inputs (the reference's int actions) and its outputs
+        acts = torch.from_numpy(rng.integers(0, 5, size=(a.e2e_steps, B, a.robots), dtype=np.int32)).pin_memory()
+        acts_np = acts.numpy()
+        outs = (torch.empty((B, a.robots, cfg.obs_dim), dtype=torch.float32).pin_memory().numpy(),
+                torch.empty((B,), dtype=torch.float64).pin_memory().numpy(),
+                torch.empty((B,), dtype=torch.uint8).pin_memory().numpy())
         hb = m.CudaEnvBatch(cfg, B, device=local, fp64=(not a.fp32), auto_reset=True)
         hb.reset_episodes(root_seed=0, first_episode=rank * B, episode_stride=world * B)
-        hb.step_host(acts[0])
+        hb.step_host(acts_np[0], out=outs)
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
         for k in range(a.e2e_steps):
-            hb.step_host(acts[k])
+            hb.step_host(acts_np[k], out=outs)
         t_e2e = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=rdev)
         if dist:
             dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
-        h2d = B * a.robots  # int8 actions
+        h2d = B * a.robots * 4  # int32 actions (std::vector<int>)
         d2h = B * a.robots * cfg.obs_dim * 4 + B * 8 + B
         e2e = {"value": world * B * a.e2e_steps / float(t_e2e.item()), "unit": "env-steps/s",
                "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
-               "api": "mrsim_step_host (host buffers, synchronous)"}
+               "api": "mrsim_step_host (pinned host buffers, synchronous)"}
         hb.close()
 
     if rank == 0:

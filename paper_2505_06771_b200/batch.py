@@ -220,12 +220,17 @@ class CudaEnvBatch:
         self._check(lib().mrsim_step(self._h, a, ptr(obs), ptr(rew), ptr(done), ptr(nxt), _stream_handle(stream)))
         return StepOutputs(obs, rew, done, nxt)
 
-    def step_host(self, actions):
-        """Synchronous step with host buffers (the reference's std::vector<int> actions)."""
+    def step_host(self, actions, out=None):
+        """Synchronous step with host buffers (the reference's std::vector<int> actions).
+        `out` = (obs float32 [B,N,D], reward float64 [B], done uint8 [B]) reuses caller
+        buffers (pinned ones make the copies run at full link speed)."""
         a = np.ascontiguousarray(np.asarray(actions, dtype=np.int32).reshape(self.num_envs, self.N))
-        obs = np.empty((self.num_envs, self.N, self.D), dtype=np.float32)
-        rew = np.empty((self.num_envs,), dtype=np.float64)
-        done = np.empty((self.num_envs,), dtype=np.uint8)
+        if out is None:
+            obs = np.empty((self.num_envs, self.N, self.D), dtype=np.float32)
+            rew = np.empty((self.num_envs,), dtype=np.float64)
+            done = np.empty((self.num_envs,), dtype=np.uint8)
+        else:
+            obs, rew, done = out
         self._check(lib().mrsim_step_host(
             self._h, a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
             obs.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), rew.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),

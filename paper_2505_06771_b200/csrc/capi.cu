@@ -49,7 +49,8 @@ struct mrsim_ctx {
     float* d_obs = nullptr;
     double* d_reward64 = nullptr;
     uint8_t* d_done = nullptr;
-    int8_t* h_actions = nullptr;  // pinned
+    int8_t* h_actions = nullptr;  // pinned (unused since the int32 upload)
+    int32_t* d_actions32 = nullptr;
     bool reset_done = false;
     // on-device feedforward policy (mrsim_set_policy_feedforward)
     bool ff = false;
@@ -242,7 +243,7 @@ int err_code(unsigned code) {
 }
 
 // Read the sticky device error word; returns MRSIM_OK or the mapped code.
-int check_device_error(mrsim_ctx* ctx, bool rollback) {
+int check_device_error(mrsim_ctx* ctx, bool rollback, const int32_t* host_actions = nullptr) {
     unsigned long long w = 0;
     long long ser = -1;
     cudaError_t e = cudaMemcpy(&w, ctx->d_err, sizeof w, cudaMemcpyDeviceToHost);
@@ -254,9 +255,10 @@ int check_device_error(mrsim_ctx* ctx, bool rollback) {
     const int robot = static_cast<int>((w >> 16) & 0xff);
     const long long env = static_cast<long long>(w >> 24);
     char buf[256];
-    if (code == mrsim_dev::kErrInvalidAction)
+    if (code == mrsim_dev::kErrInvalidAction)  // the device keeps 8 bits; the host buffer has the full value
         std::snprintf(buf, sizeof buf, "step_batch: invalid action %d for environment %lld, robot %d",
-                      static_cast<int8_t>(detail), env, robot);
+                      host_actions ? host_actions[env * ctx->N + robot] : static_cast<int>(static_cast<int8_t>(detail)),
+                      env, robot);
     else if (code == mrsim_dev::kErrSpawn)
         std::snprintf(buf, sizeof buf, "sample_poses: could not place robot %d after 1000 attempts (environment %lld)",
                       robot, env);
@@ -273,7 +275,7 @@ int check_device_error(mrsim_ctx* ctx, bool rollback) {
 
 template <class Real>
 int do_step(mrsim_ctx* ctx, DevState<Real>* s, const int8_t* actions, float* obs, float* reward, uint8_t* done,
-            float* next_obs, cudaStream_t stream, double* reward64 = nullptr) {
+            float* next_obs, cudaStream_t stream, double* reward64 = nullptr, const int32_t* actions32 = nullptr) {
     StepParams<Real> p;
     std::memset(&p, 0, sizeof p);
     p.c = ctx->cfg;
@@ -281,6 +283,7 @@ int do_step(mrsim_ctx* ctx, DevState<Real>* s, const int8_t* actions, float* obs
     p.out = s[1 - ctx->cur];
     p.st = ctx->st;
     p.actions = actions;
+    p.actions32 = actions32;
     p.obs = obs;
     p.reward = reward;
     p.reward64 = reward64;
@@ -723,6 +726,7 @@ void mrsim_destroy(mrsim_ctx* ctx) {
     cudaFree(ctx->stats_mem);
     cudaFree(ctx->d_err);
     cudaFree(ctx->d_actions);
+    cudaFree(ctx->d_actions32);
     cudaFree(ctx->d_obs);
     cudaFree(ctx->d_reward64);
     cudaFree(ctx->d_done);
@@ -803,34 +807,25 @@ int mrsim_step_host(mrsim_ctx* ctx, const int32_t* actions_host, float* obs_host
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const long long BN = ctx->B * ctx->N;
     const size_t obs_bytes = sizeof(float) * BN * ctx->D;
-    if (!ctx->d_actions) CK(cudaMalloc(&ctx->d_actions, BN));
+    if (!ctx->d_actions32) CK(cudaMalloc(&ctx->d_actions32, 4 * BN));
     if (!ctx->d_obs) CK(cudaMalloc(&ctx->d_obs, obs_bytes));
     if (!ctx->d_reward64) CK(cudaMalloc(&ctx->d_reward64, 8 * ctx->B));
     if (!ctx->d_done) CK(cudaMalloc(&ctx->d_done, ctx->B));
-    if (!ctx->h_actions) CK(cudaMallocHost(&ctx->h_actions, BN));
-    // validate_actions (batch.hpp:226-237): sequential, first offender reported
-    for (long long k = 0; k < BN; ++k) {
-        const int a = actions_host[k];
-        if (a < 0 || a >= 5) {
-            char buf[160];
-            std::snprintf(buf, sizeof buf, "step_batch: invalid action %d for environment %lld, robot %lld", a,
-                          k / ctx->N, k % ctx->N);
-            return set_err(ctx, MRSIM_E_INVALID_ARGUMENT, buf);
-        }
-        ctx->h_actions[k] = static_cast<int8_t>(a);
-    }
-    CK(cudaMemcpyAsync(ctx->d_actions, ctx->h_actions, BN, cudaMemcpyHostToDevice, s));
-    int rc = ctx->fp64 ? do_step<double>(ctx, ctx->sd, ctx->d_actions, obs_host ? ctx->d_obs : nullptr, nullptr,
+    // The reference's std::vector<int> goes up as is; validate_actions (batch.hpp:226-237) runs in the
+    // step kernel (first offender in (env, robot) order wins), and a failing step is rolled back below.
+    CK(cudaMemcpyAsync(ctx->d_actions32, actions_host, 4 * BN, cudaMemcpyHostToDevice, s));
+    int rc = ctx->fp64 ? do_step<double>(ctx, ctx->sd, nullptr, obs_host ? ctx->d_obs : nullptr, nullptr,
                                          done_host ? ctx->d_done : nullptr, nullptr, s,
-                                         reward_host ? ctx->d_reward64 : nullptr)
-                       : do_step<float>(ctx, ctx->sf, ctx->d_actions, obs_host ? ctx->d_obs : nullptr, nullptr,
+                                         reward_host ? ctx->d_reward64 : nullptr, ctx->d_actions32)
+                       : do_step<float>(ctx, ctx->sf, nullptr, obs_host ? ctx->d_obs : nullptr, nullptr,
                                         done_host ? ctx->d_done : nullptr, nullptr, s,
-                                        reward_host ? ctx->d_reward64 : nullptr);
+                                        reward_host ? ctx->d_reward64 : nullptr, ctx->d_actions32);
     if (rc != MRSIM_OK) return rc;
     if (obs_host) CK(cudaMemcpyAsync(obs_host, ctx->d_obs, obs_bytes, cudaMemcpyDeviceToHost, s));
     if (reward_host) CK(cudaMemcpyAsync(reward_host, ctx->d_reward64, 8 * ctx->B, cudaMemcpyDeviceToHost, s));
     if (done_host) CK(cudaMemcpyAsync(done_host, ctx->d_done, ctx->B, cudaMemcpyDeviceToHost, s));
-    return mrsim_sync(ctx, stream);
+    CK(cudaStreamSynchronize(s));
+    return check_device_error(ctx, true, actions_host);
 }
 
 int mrsim_observe(mrsim_ctx* ctx, float* obs_dev, void* stream) {

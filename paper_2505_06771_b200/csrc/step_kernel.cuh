@@ -26,8 +26,11 @@
 #ifndef MRSIM_RW_MINB
 #define MRSIM_RW_MINB 3
 #endif
+#ifndef MRSIM_SMALL_MINB
+#define MRSIM_SMALL_MINB 4
+#endif
 #ifndef MRSIM_MIN_BLOCKS
-#define MRSIM_MIN_BLOCKS(L, TASK) ((L) >= 16 ? 3 : (TASK) == MRSIM_TASK_RWARE ? MRSIM_RW_MINB : 4)
+#define MRSIM_MIN_BLOCKS(L, TASK) ((L) >= 16 ? 3 : (TASK) == MRSIM_TASK_RWARE ? MRSIM_RW_MINB : MRSIM_SMALL_MINB)
 #endif
 
 namespace mrsim_dev {
@@ -67,7 +70,8 @@ struct StepParams {
     mrsim_cfg c;
     DevState<Real> in, out;
     EnvStats st;
-    const int8_t* actions;  // [B][N] or nullptr (on-device random policy)
+    const int8_t* actions;     // [B][N] or nullptr (on-device random policy)
+    const int32_t* actions32;  // [B][N] the host API's std::vector<int> actions, used when actions is null
     float* obs;             // [B][N][D] or nullptr
     float* reward;          // [B] or nullptr
     double* reward64;       // [B] or nullptr (host-API path: the reference's double team reward)
@@ -493,7 +497,9 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
 
         // ---- actions (validate_actions, batch.hpp:226-237) ----
         int act = 0;
-        if (vl) act = p.actions ? static_cast<int>(p.actions[e * N + ri]) : policy_action(p.in.pkey[e], step_index, ri);
+        if (vl)
+            act = p.actions ? static_cast<int>(p.actions[e * N + ri])
+                            : (p.actions32 ? p.actions32[e * N + ri] : policy_action(p.in.pkey[e], step_index, ri));
         const int bad_robot = g.first(vl && (act < 0 || act >= 5));
         const int bad_act = g.shfl(act, bad_robot < 0 ? 0 : bad_robot);
         if (bad_robot >= 0 && lane == 0 && !ghost) {

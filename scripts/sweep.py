@@ -9,7 +9,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CONFIGS = [("navigation", 4, 65536), ("predator_prey", 6, 32768), ("discovery", 6, 32768), ("rware", 4, 65536),
            ("rware", 6, 65536), ("foraging", 4, 65536), ("foraging", 6, 65536), ("material_transport", 10, 131072),
-           ("arctic_transport", 10, 131072), ("warehouse", 4, 65536)]
+           ("arctic_transport", 10, 131072), ("warehouse", 4, 65536), ("random_waypoints", 4, 65536)]
 
 
 def run(args):
