@@ -5,6 +5,7 @@
 // launches the sm_100a kernels or fails with MRSIM_E_CUDA.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -44,12 +45,14 @@ struct mrsim_ctx {
     int block = 128;
     int grid = 0;
     int smem_group = 0;
+    int obs_stage = 0;  // floats per warp of the staged obs store (0: direct stores)
     // host-API scratch
     int8_t* d_actions = nullptr;
     float* d_obs = nullptr;
     double* d_reward64 = nullptr;
     uint8_t* d_done = nullptr;
     int8_t* h_actions = nullptr;  // pinned (unused since the int32 upload)
+    unsigned long long* h_err = nullptr;  // pinned copy of the device error word + serial
     int32_t* d_actions32 = nullptr;
     bool reset_done = false;
     // on-device feedforward policy (mrsim_set_policy_feedforward)
@@ -243,13 +246,20 @@ int err_code(unsigned code) {
 }
 
 // Read the sticky device error word; returns MRSIM_OK or the mapped code.
-int check_device_error(mrsim_ctx* ctx, bool rollback, const int32_t* host_actions = nullptr) {
+int check_device_error(mrsim_ctx* ctx, bool rollback, const int32_t* host_actions = nullptr,
+                       const unsigned long long* fetched = nullptr) {
     unsigned long long w = 0;
     long long ser = -1;
-    cudaError_t e = cudaMemcpy(&w, ctx->d_err, sizeof w, cudaMemcpyDeviceToHost);
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "read device error");
-    if (w == ~0ull) return MRSIM_OK;
-    cudaMemcpy(&ser, ctx->d_err_serial, sizeof ser, cudaMemcpyDeviceToHost);
+    if (fetched) {  // error word + serial already copied to host with the step's outputs
+        w = fetched[0];
+        if (w == ~0ull) return MRSIM_OK;
+        ser = static_cast<long long>(fetched[1]);
+    } else {
+        cudaError_t e = cudaMemcpy(&w, ctx->d_err, sizeof w, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "read device error");
+        if (w == ~0ull) return MRSIM_OK;
+        cudaMemcpy(&ser, ctx->d_err_serial, sizeof ser, cudaMemcpyDeviceToHost);
+    }
     const unsigned code = static_cast<unsigned>(w & 0xff);
     const int detail = static_cast<int>((w >> 8) & 0xff);
     const int robot = static_cast<int>((w >> 16) & 0xff);
@@ -274,8 +284,8 @@ int check_device_error(mrsim_ctx* ctx, bool rollback, const int32_t* host_action
 }
 
 template <class Real>
-int do_step(mrsim_ctx* ctx, DevState<Real>* s, const int8_t* actions, float* obs, float* reward, uint8_t* done,
-            float* next_obs, cudaStream_t stream, double* reward64 = nullptr, const int32_t* actions32 = nullptr) {
+StepParams<Real> step_params(mrsim_ctx* ctx, DevState<Real>* s, const int8_t* actions, float* obs, float* reward,
+                             uint8_t* done, float* next_obs, double* reward64, const int32_t* actions32) {
     StepParams<Real> p;
     std::memset(&p, 0, sizeof p);
     p.c = ctx->cfg;
@@ -293,6 +303,8 @@ int do_step(mrsim_ctx* ctx, DevState<Real>* s, const int8_t* actions, float* obs
     p.err_serial = ctx->d_err_serial;
     p.serial = ctx->serial;
     p.B = ctx->B;
+    p.e_begin = 0;
+    p.e_end = ctx->B;
     p.N = ctx->N;
     p.n = ctx->n;
     p.P = ctx->P;
@@ -304,16 +316,45 @@ int do_step(mrsim_ctx* ctx, DevState<Real>* s, const int8_t* actions, float* obs
     p.root_seed = ctx->root_seed;
     p.episode_stride = ctx->episode_stride;
     p.smem_bytes_per_group = ctx->smem_group;
+    p.obs_stage = ctx->obs_stage;
     mrsim_host::fill_consts(ctx->cfg, p.k);
     mrsim_dev::prey_offsets(ctx->cfg, p.prey_off);
-    const int smem = ctx->smem_group * (ctx->block / ctx->L);
-    cudaError_t e = dispatch_step<Real>(ctx->cfg.task, p, ctx->var, ctx->grid, ctx->block, smem, stream);
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "step kernel launch");
+    return p;
+}
+
+// Bookkeeping after every env of a step has been launched (ping-pong flip, rollback history).
+void step_done(mrsim_ctx* ctx) {
     ctx->hist_in[ctx->serial % 64] = ctx->cur;
     ctx->serial += 1;
     ctx->cur = 1 - ctx->cur;
     ctx->env_steps += ctx->B;
+}
+
+template <class Real>
+int do_step(mrsim_ctx* ctx, DevState<Real>* s, const int8_t* actions, float* obs, float* reward, uint8_t* done,
+            float* next_obs, cudaStream_t stream, double* reward64 = nullptr, const int32_t* actions32 = nullptr) {
+    const StepParams<Real> p = step_params<Real>(ctx, s, actions, obs, reward, done, next_obs, reward64, actions32);
+    const int smem = ctx->smem_group * (ctx->block / ctx->L) + 4 * ctx->obs_stage * (ctx->block / 32);
+    cudaError_t e = dispatch_step<Real>(ctx->cfg.task, p, ctx->var, ctx->grid, ctx->block, smem, stream);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "step kernel launch");
+    step_done(ctx);
     return MRSIM_OK;
+}
+
+// Device-accessible alias of a host pointer: page-locked (pinned) host memory
+// is mapped into the device address space, so the step kernel can read the
+// actions and write obs / reward / done straight over the host link while it
+// computes (no separate copy phase). nullptr for pageable memory.
+template <class T>
+T* mapped_alias(T* host) {
+    if (!host) return nullptr;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, host) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (a.type != cudaMemoryTypeHost || !a.devicePointer) return nullptr;
+    return static_cast<T*>(a.devicePointer);
 }
 
 template <class Real>
@@ -710,6 +751,17 @@ int mrsim_create(const mrsim_cfg* cfg, int device, int64_t num_envs, uint32_t fl
                   : dispatch_occ<float>(cfg->task, ctx->var, ctx->block, smem, &bps);
     if (e != cudaSuccess) return bail(e, "occupancy query");
     if (bps < 1) bps = 1;
+    // Warp-staged observation stores (one contiguous block per warp, full-line writes; what makes
+    // zero-copy obs to pinned host memory efficient): on when it costs no occupancy.
+    {
+        const int stage = (32 / ctx->L) * ctx->N * ctx->D;  // floats per warp
+        const int smem2 = smem + 4 * stage * (ctx->block / 32);
+        int bps2 = 0;
+        e = ctx->fp64 ? dispatch_occ<double>(cfg->task, ctx->var, ctx->block, smem2, &bps2)
+                      : dispatch_occ<float>(cfg->task, ctx->var, ctx->block, smem2, &bps2);
+        if (e != cudaSuccess) return bail(e, "occupancy query");
+        ctx->obs_stage = (bps2 >= bps) ? stage : 0;
+    }
     const long long gpb = ctx->block / ctx->L;
     const long long need = (ctx->B + gpb - 1) / gpb;
     const long long full = static_cast<long long>(ctx->num_sms) * bps;
@@ -731,6 +783,7 @@ void mrsim_destroy(mrsim_ctx* ctx) {
     cudaFree(ctx->d_reward64);
     cudaFree(ctx->d_done);
     if (ctx->h_actions) cudaFreeHost(ctx->h_actions);
+    if (ctx->h_err) cudaFreeHost(ctx->h_err);
     cudaFree(ctx->d_wT);
     cudaFree(ctx->d_bias);
     cudaFree(ctx->d_pol_actions);
@@ -807,25 +860,41 @@ int mrsim_step_host(mrsim_ctx* ctx, const int32_t* actions_host, float* obs_host
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const long long BN = ctx->B * ctx->N;
     const size_t obs_bytes = sizeof(float) * BN * ctx->D;
-    if (!ctx->d_actions32) CK(cudaMalloc(&ctx->d_actions32, 4 * BN));
-    if (!ctx->d_obs) CK(cudaMalloc(&ctx->d_obs, obs_bytes));
-    if (!ctx->d_reward64) CK(cudaMalloc(&ctx->d_reward64, 8 * ctx->B));
-    if (!ctx->d_done) CK(cudaMalloc(&ctx->d_done, ctx->B));
+    // pinned caller buffers are used in place by the kernel (zero-copy); pageable ones are staged
+    const int32_t* act = mapped_alias(actions_host);
+    float* obs = mapped_alias(obs_host);
+    double* rew = mapped_alias(reward_host);
+    uint8_t* done = mapped_alias(done_host);
+    if (!act) {
+        if (!ctx->d_actions32) CK(cudaMalloc(&ctx->d_actions32, 4 * BN));
+        CK(cudaMemcpyAsync(ctx->d_actions32, actions_host, 4 * BN, cudaMemcpyHostToDevice, s));
+        act = ctx->d_actions32;
+    }
+    if (obs_host && !obs) {
+        if (!ctx->d_obs) CK(cudaMalloc(&ctx->d_obs, obs_bytes));
+        obs = ctx->d_obs;
+    }
+    if (reward_host && !rew) {
+        if (!ctx->d_reward64) CK(cudaMalloc(&ctx->d_reward64, 8 * ctx->B));
+        rew = ctx->d_reward64;
+    }
+    if (done_host && !done) {
+        if (!ctx->d_done) CK(cudaMalloc(&ctx->d_done, ctx->B));
+        done = ctx->d_done;
+    }
     // The reference's std::vector<int> goes up as is; validate_actions (batch.hpp:226-237) runs in the
     // step kernel (first offender in (env, robot) order wins), and a failing step is rolled back below.
-    CK(cudaMemcpyAsync(ctx->d_actions32, actions_host, 4 * BN, cudaMemcpyHostToDevice, s));
-    int rc = ctx->fp64 ? do_step<double>(ctx, ctx->sd, nullptr, obs_host ? ctx->d_obs : nullptr, nullptr,
-                                         done_host ? ctx->d_done : nullptr, nullptr, s,
-                                         reward_host ? ctx->d_reward64 : nullptr, ctx->d_actions32)
-                       : do_step<float>(ctx, ctx->sf, nullptr, obs_host ? ctx->d_obs : nullptr, nullptr,
-                                        done_host ? ctx->d_done : nullptr, nullptr, s,
-                                        reward_host ? ctx->d_reward64 : nullptr, ctx->d_actions32);
+    const int rc = ctx->fp64 ? do_step<double>(ctx, ctx->sd, nullptr, obs, nullptr, done, nullptr, s, rew, act)
+                             : do_step<float>(ctx, ctx->sf, nullptr, obs, nullptr, done, nullptr, s, rew, act);
     if (rc != MRSIM_OK) return rc;
-    if (obs_host) CK(cudaMemcpyAsync(obs_host, ctx->d_obs, obs_bytes, cudaMemcpyDeviceToHost, s));
-    if (reward_host) CK(cudaMemcpyAsync(reward_host, ctx->d_reward64, 8 * ctx->B, cudaMemcpyDeviceToHost, s));
-    if (done_host) CK(cudaMemcpyAsync(done_host, ctx->d_done, ctx->B, cudaMemcpyDeviceToHost, s));
+    if (obs_host && obs == ctx->d_obs) CK(cudaMemcpyAsync(obs_host, obs, obs_bytes, cudaMemcpyDeviceToHost, s));
+    if (reward_host && rew == ctx->d_reward64)
+        CK(cudaMemcpyAsync(reward_host, rew, 8 * ctx->B, cudaMemcpyDeviceToHost, s));
+    if (done_host && done == ctx->d_done) CK(cudaMemcpyAsync(done_host, done, ctx->B, cudaMemcpyDeviceToHost, s));
+    if (!ctx->h_err) CK(cudaMallocHost(&ctx->h_err, 16));
+    CK(cudaMemcpyAsync(ctx->h_err, ctx->d_err, 16, cudaMemcpyDeviceToHost, s));  // error word + serial
     CK(cudaStreamSynchronize(s));
-    return check_device_error(ctx, true, actions_host);
+    return check_device_error(ctx, true, actions_host, ctx->h_err);
 }
 
 int mrsim_observe(mrsim_ctx* ctx, float* obs_dev, void* stream) {

@@ -81,11 +81,13 @@ struct StepParams {
     long long* err_serial;
     long long serial;
     long long B;
+    long long e_begin, e_end;  // env range of this launch (the host API pipelines chunks of a step)
     int N, n, P, D, bdim, nf, ni;
     int auto_reset;
     uint64_t root_seed;
     long long episode_stride;
     int smem_bytes_per_group;
+    int obs_stage;  // floats per warp of the obs staging buffer after the group regions (0: direct stores)
     PhysConsts<Real> k;
     double prey_off[16];  // predator_prey candidate offsets (host-computed with the reference's libm)
 };
@@ -483,10 +485,11 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
     const EnvView<Real> view{sm.xs, sm.ys, sm.ts, sm.tf, sm.ti, N, sm.drones, p.prey_off};
     const long long stride = static_cast<long long>(gridDim.x) * gpb;
 
-    for (long long e0 = static_cast<long long>(blockIdx.x) * gpb + (gib & ~(G - 1)); e0 < p.B; e0 += stride) {
+    for (long long e0 = p.e_begin + static_cast<long long>(blockIdx.x) * gpb + (gib & ~(G - 1)); e0 < p.e_end;
+         e0 += stride) {
         const long long e_real = e0 + (gib & (G - 1));
-        const bool ghost = e_real >= p.B;
-        const long long e = ghost ? p.B - 1 : e_real;
+        const bool ghost = e_real >= p.e_end;
+        const long long e = ghost ? p.e_end - 1 : e_real;
         // ---- load ----
         const int step_index = p.in.step_index[e];
         const uint64_t key = p.in.key[e];
@@ -713,7 +716,23 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
 
         // ---- observations (assemble_observations, batch.hpp:143-151) ----
         const int ND = N * p.D;
-        if (p.obs && !skip) {
+        if (p.obs && p.obs_stage) {
+            // the warp's G envs are consecutive: stage their obs, then store one contiguous block
+            // (every store instruction writes 128 contiguous bytes)
+            float* wst = reinterpret_cast<float*>(smem_raw + gpb * p.smem_bytes_per_group) +
+                         (threadIdx.x >> 5) * p.obs_stage;
+            float* mine = wst + (gib & (G - 1)) * ND;
+            for (int q = lane; q < ND; q += L) {
+                const int r = q / p.D;
+                mine[q] = static_cast<float>(obs_feature<TASK, Real>(c, view, r, q - r * p.D, p.bdim));
+            }
+            __syncwarp();
+            const long long left = p.e_end - e0;
+            const int total = static_cast<int>(left < G ? left : G) * ND;
+            float* dst = p.obs + e0 * ND;
+            for (int k = threadIdx.x & 31; k < total; k += 32) dst[k] = wst[k];
+            __syncwarp();
+        } else if (p.obs && !skip) {
             float* o = p.obs + e * ND;
             for (int q = lane; q < ND; q += L) {
                 const int r = q / p.D;

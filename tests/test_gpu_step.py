@@ -273,3 +273,44 @@ def test_identical_instances_and_purity():
     assert list(s[0].x[:3]) == list(s[1].x[:3])
     assert rew[0] == rew[1] and rew[2] != rew[0]
     assert np.array_equal(obs[0], obs[1])
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_host_api_matches_device_step(pinned):
+    """mrsim_step_host with pageable buffers (staged copies) or pinned ones (the
+    kernel reads actions / writes outputs in place over the host link) equals
+    the device-buffer step."""
+    import torch
+    cfg = m.make_default_config("navigation")
+    cfg.set_num_robots(4)
+    B = 50000
+    seeds = [m.derive_episode_seed(12, e) for e in range(B)]
+    ga, gb = m.CudaEnvBatch(cfg, B), m.CudaEnvBatch(cfg, B)
+    ga.reset_seeds(seeds)
+    gb.reset_seeds(seeds)
+    rng = np.random.default_rng(0)
+
+    def buf(shape, dt):
+        t = torch.empty(shape, dtype=dt)
+        return (t.pin_memory() if pinned else t).numpy()
+
+    outs = (buf((B, 4, cfg.obs_dim), torch.float32), buf((B,), torch.float64), buf((B,), torch.uint8))
+    act_buf = buf((B, 4), torch.int32)
+    for t in range(3):
+        act_buf[:] = rng.integers(0, 5, size=(B, 4), dtype=np.int32)
+        acts = act_buf
+        obs, rew, done = ga.step_host(acts, out=outs)
+        out = gb.step(torch.from_numpy(acts.astype(np.int8)).cuda())
+        torch.cuda.synchronize()
+        assert np.array_equal(obs, out.obs.cpu().numpy())
+        assert np.array_equal(rew.astype(np.float32), out.reward.cpu().numpy())
+        assert np.array_equal(done, out.done.cpu().numpy())
+    sa, sb = ga.get_states(), gb.get_states()
+    for e in (0, 18943, 18944, 37888, B - 1):
+        assert list(sa[e].x[:4]) == list(sb[e].x[:4]) and sa[e].step_index == sb[e].step_index
+    act_buf[:] = rng.integers(0, 5, size=(B, 4), dtype=np.int32)
+    act_buf[40000, 2] = 300  # reported with its full value, the step rolled back
+    before = ga.get_states(40000, 1)[0].x[0]
+    with pytest.raises(m.InvalidArgument, match=r"invalid action 300 for environment 40000, robot 2"):
+        ga.step_host(act_buf, out=outs)
+    assert ga.get_states(40000, 1)[0].x[0] == before
