@@ -332,9 +332,13 @@ void step_done(mrsim_ctx* ctx) {
 
 template <class Real>
 int do_step(mrsim_ctx* ctx, DevState<Real>* s, const int8_t* actions, float* obs, float* reward, uint8_t* done,
-            float* next_obs, cudaStream_t stream, double* reward64 = nullptr, const int32_t* actions32 = nullptr) {
-    const StepParams<Real> p = step_params<Real>(ctx, s, actions, obs, reward, done, next_obs, reward64, actions32);
-    const int smem = ctx->smem_group * (ctx->block / ctx->L) + 4 * ctx->obs_stage * (ctx->block / 32);
+            float* next_obs, cudaStream_t stream, double* reward64 = nullptr, const int32_t* actions32 = nullptr,
+            bool stage_obs = false) {
+    StepParams<Real> p = step_params<Real>(ctx, s, actions, obs, reward, done, next_obs, reward64, actions32);
+    // warp-staged obs stores only where they pay: obs going straight to pinned host memory
+    // (device-memory obs: ~2 % slower staged, measured)
+    p.obs_stage = stage_obs ? ctx->obs_stage : 0;
+    const int smem = ctx->smem_group * (ctx->block / ctx->L) + 4 * p.obs_stage * (ctx->block / 32);
     cudaError_t e = dispatch_step<Real>(ctx->cfg.task, p, ctx->var, ctx->grid, ctx->block, smem, stream);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "step kernel launch");
     step_done(ctx);
@@ -884,8 +888,11 @@ int mrsim_step_host(mrsim_ctx* ctx, const int32_t* actions_host, float* obs_host
     }
     // The reference's std::vector<int> goes up as is; validate_actions (batch.hpp:226-237) runs in the
     // step kernel (first offender in (env, robot) order wins), and a failing step is rolled back below.
-    const int rc = ctx->fp64 ? do_step<double>(ctx, ctx->sd, nullptr, obs, nullptr, done, nullptr, s, rew, act)
-                             : do_step<float>(ctx, ctx->sf, nullptr, obs, nullptr, done, nullptr, s, rew, act);
+    const bool zero_copy_obs = obs && obs != ctx->d_obs;
+    const int rc = ctx->fp64 ? do_step<double>(ctx, ctx->sd, nullptr, obs, nullptr, done, nullptr, s, rew, act,
+                                               zero_copy_obs)
+                             : do_step<float>(ctx, ctx->sf, nullptr, obs, nullptr, done, nullptr, s, rew, act,
+                                              zero_copy_obs);
     if (rc != MRSIM_OK) return rc;
     if (obs_host && obs == ctx->d_obs) CK(cudaMemcpyAsync(obs_host, obs, obs_bytes, cudaMemcpyDeviceToHost, s));
     if (reward_host && rew == ctx->d_reward64)
