@@ -408,12 +408,12 @@ template <class Real>
 struct GroupSmem {
     QpWs<Real, BarrierDesc<Real>> qp;
     Real *xs, *ys, *ts, *tf, *rc;
-    int *ti, *misc, *drones;
+    int *ti, *misc, *drones, *dcell;
     static __host__ __device__ int rc_reals(int L, int MP, int MO) { return (3 * MP + 4 + 3 * MO + 2) * L; }
     static __host__ __device__ int bytes(int N, int nf, int ni, int L, int MP, int MO) {
         const int qb = (QpWs<Real, BarrierDesc<Real>>::bytes(2 * N) + 15) & ~15;
         const int reals = 3 * N + nf + rc_reals(L, MP, MO);
-        const int ints = ni + 2 + N;
+        const int ints = ni + 2 + N + 2 * N;  // task words, misc, drone list, drone cells
         const int b = qb + reals * static_cast<int>(sizeof(Real)) + ints * 4;
         return (b + 15) & ~15;
     }
@@ -474,7 +474,9 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
     sm.carve(smem_raw + gib * p.smem_bytes_per_group, N, p.nf, GroupSmem<Real>::rc_reals(L, MP, MO));
     int* misc = sm.ti + p.ni;
     sm.drones = misc + 2;
-    if (TASK == MRSIM_TASK_ARCTIC_TRANSPORT && lane == 0) arctic_drones(c, sm.drones);
+    sm.dcell = sm.drones + N;
+    int n_drones = 0;
+    if (TASK == MRSIM_TASK_ARCTIC_TRANSPORT) n_drones = arctic_drones(c, sm.drones);
 
     const bool vl = lane < N;  // lane r carries robot r
     const int ri = vl ? lane : 0;
@@ -482,7 +484,8 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
     BarrierRows<Real, L, MP, MO> rows;
     init_rows(rows, sm.rc, lane, N, p.k.cap);
     const int total_rows_base = rows.P + 4 * N + 4 * N;
-    const EnvView<Real> view{sm.xs, sm.ys, sm.ts, sm.tf, sm.ti, N, sm.drones, p.prey_off};
+    const EnvView<Real> view{sm.xs, sm.ys, sm.ts, sm.tf, sm.ti, N, sm.drones, p.prey_off,
+                             TASK == MRSIM_TASK_ARCTIC_TRANSPORT ? sm.dcell : nullptr};
     const long long stride = static_cast<long long>(gridDim.x) * gpb;
 
     for (long long e0 = p.e_begin + static_cast<long long>(blockIdx.x) * gpb + (gib & ~(G - 1)); e0 < p.e_end;
@@ -715,6 +718,13 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
         const int done = misc[0];
 
         // ---- observations (assemble_observations, batch.hpp:143-151) ----
+        if (TASK == MRSIM_TASK_ARCTIC_TRANSPORT) {  // each drone's cell once, not once per patch feature
+            if (lane < n_drones) {
+                const int d = sm.drones[lane];
+                arctic_cell<Real>(c, sm.xs[d], sm.ys[d], sm.dcell[2 * lane], sm.dcell[2 * lane + 1]);
+            }
+            Grp<L>::sync();
+        }
         const int ND = N * p.D;
         if (p.obs && p.obs_stage) {
             // the warp's G envs are consecutive: stage their obs, then store one contiguous block
@@ -775,10 +785,12 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
         }
         Grp<L>::sync();
         if (p.auto_reset && done && !skip && p.next_obs) {
+            EnvView<Real> fresh = view;  // the drone-cell cache holds the terminal poses
+            fresh.dcell = nullptr;
             float* o = p.next_obs + e * ND;
             for (int q = lane; q < ND; q += L) {
                 const int r = q / p.D;
-                o[q] = static_cast<float>(obs_feature<TASK, Real>(c, view, r, q - r * p.D, p.bdim));
+                o[q] = static_cast<float>(obs_feature<TASK, Real>(c, fresh, r, q - r * p.D, p.bdim));
             }
         }
 

@@ -252,7 +252,20 @@ struct EnvView {
     int N;
     const int* drones;  // arctic: robot index of the k-th drone (robot-index order), else unused
     const double* prey_off;  // predator_prey: 8 candidate offsets (x, y), else unused
+    const int* dcell = nullptr;  // arctic: (col, row) of the k-th drone, cached per env (or null)
 };
+
+// arctic: the grid cell under a robot, with the observation's truncating casts
+// (arctic_transport.hpp:206-209); used per drone for its 3x3 patch.
+template <class Real>
+__device__ __forceinline__ void arctic_cell(const mrsim_cfg& c, Real x, Real y, int& c0, int& r0) {
+    const int cols = c.layout.arctic_grid_cols, rows = c.layout.arctic_grid_rows;
+    const Real hw = Real(c.arena_half_width), hh = Real(c.arena_half_height);
+    const Real cw = (hw - (-hw)) / Real(cols);
+    const Real ch = (hh - (-hh)) / Real(rows);
+    c0 = static_cast<int>(dclamp((x - (-hw)) / cw, Real(0), Real(cols - 1)));
+    r0 = static_cast<int>(dclamp((y - (-hh)) / ch, Real(0), Real(rows - 1)));
+}
 
 // predator_prey: prey_step = agility * max step size (predator_prey.hpp:177-181) and the
 // 8 compass offsets Vec2{cos(ang), sin(ang)} * prey_step, ang = (k-1) pi/4 (predator_prey.hpp:128-133)
@@ -646,13 +659,15 @@ __device__ Real obs_feature(const mrsim_cfg& c, const EnvView<Real>& v, int r, i
         if (f == 0) return Real(arctic_tile_at<Real>(c, v.ti, v.xs[r], v.ys[r]));
         const int g2 = f - 1;
         const int which = g2 / 9, cell = g2 % 9;
-        const int d = v.drones[which];  // which-th drone in robot-index order
         const int cols = L.arctic_grid_cols, rows = L.arctic_grid_rows;
-        const Real hw = Real(c.arena_half_width), hh = Real(c.arena_half_height);
-        const Real cw = (hw - (-hw)) / Real(cols);
-        const Real ch = (hh - (-hh)) / Real(rows);
-        const int c0 = static_cast<int>(dclamp((v.xs[d] - (-hw)) / cw, Real(0), Real(cols - 1)));
-        const int r0 = static_cast<int>(dclamp((v.ys[d] - (-hh)) / ch, Real(0), Real(rows - 1)));
+        int c0, r0;
+        if (v.dcell) {
+            c0 = v.dcell[2 * which];
+            r0 = v.dcell[2 * which + 1];
+        } else {
+            const int d = v.drones[which];  // which-th drone in robot-index order
+            arctic_cell<Real>(c, v.xs[d], v.ys[d], c0, r0);
+        }
         const int rr = r0 + cell / 3 - 1, cc = c0 + cell % 3 - 1;
         const bool in = rr >= 0 && rr < rows && cc >= 0 && cc < cols;
         return in ? Real(ti_byte(v.ti, rr * cols + cc)) : Real(0);
