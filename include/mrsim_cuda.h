@@ -312,6 +312,13 @@ int mrsim_set_policy_feedforward(mrsim_ctx* ctx, int num_layers, const int32_t* 
                                  const double* weights, int greedy);
 /* Back to PolicyKind::Random (the default). */
 int mrsim_set_policy_random(mrsim_ctx* ctx);
+/* The reference's scripted policies on device: PolicyKind::ScriptedGoal (grid
+ * BFS planner toward Scenario::scripted_goal, policy.hpp:242-360) or
+ * PolicyKind::PreyChaser (policy.hpp:362-416; predator_prey only, else
+ * MRSIM_E_INVALID_ARGUMENT like resolve_scenario_config, harness.hpp:100-102). */
+#define MRSIM_POLICY_SCRIPTED_GOAL 1
+#define MRSIM_POLICY_PREY_CHASER 2
+int mrsim_set_policy_scripted(mrsim_ctx* ctx, int kind);
 /* The context policy's actions for the current step of every env (the
  * observation of the current state, i.e. the one the last reset/step
  * returned) into actions_dev [num_envs][N]. Asynchronous on `stream`. */

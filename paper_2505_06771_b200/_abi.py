@@ -108,6 +108,7 @@ FUNCTIONS = {
     "mrsim_set_policy_feedforward": (ctypes.c_int, [c_void_p, ctypes.c_int, P(ctypes.c_int32), P(ctypes.c_int32),
                                                     P(ctypes.c_double), ctypes.c_int]),
     "mrsim_set_policy_random": (ctypes.c_int, [c_void_p]),
+    "mrsim_set_policy_scripted": (ctypes.c_int, [c_void_p, ctypes.c_int]),
     "mrsim_policy_actions": (ctypes.c_int, [c_void_p, c_void_p, c_void_p]),
     "mrsim_sync": (ctypes.c_int, [c_void_p, c_void_p]),
     "mrsim_capture_begin": (ctypes.c_int, [c_void_p, ctypes.c_int64]),

@@ -250,12 +250,19 @@ class CudaEnvBatch:
 
     # -- on-device policy (Policy, policy.hpp:432-486) --
     def set_policy(self, spec):
-        """PolicySpec forms (policy.hpp:24-47): "random", "feedforward:<path>",
-        "feedforward_sample:<path>", or a FeedforwardWeights (greedy)."""
+        """PolicySpec forms (policy.hpp:24-47): "random", "scripted_goal" (or "scripted"),
+        "prey_chaser", "feedforward:<path>", "feedforward_sample:<path>", or a
+        FeedforwardWeights (greedy)."""
         if isinstance(spec, FeedforwardWeights):
             return self.set_feedforward(spec, greedy=True)
         if spec == "random":
             self._check(lib().mrsim_set_policy_random(self._h))
+            return self
+        if spec in ("scripted_goal", "scripted"):
+            self._check(lib().mrsim_set_policy_scripted(self._h, _abi.MRSIM_POLICY_SCRIPTED_GOAL))
+            return self
+        if spec == "prey_chaser":
+            self._check(lib().mrsim_set_policy_scripted(self._h, _abi.MRSIM_POLICY_PREY_CHASER))
             return self
         for prefix, greedy in (("feedforward:", True), ("feedforward_sample:", False)):
             if spec.startswith(prefix):

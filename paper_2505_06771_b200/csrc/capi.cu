@@ -55,7 +55,8 @@ struct mrsim_ctx {
     unsigned long long* h_err = nullptr;  // pinned copy of the device error word + serial
     int32_t* d_actions32 = nullptr;
     bool reset_done = false;
-    // on-device feedforward policy (mrsim_set_policy_feedforward)
+    // on-device policy: feedforward network (mrsim_set_policy_feedforward) or scripted (kind != 0)
+    int scripted = 0;
     bool ff = false;
     mrsim_dev::PolicyNet net{};
     double* d_wT = nullptr;
@@ -189,7 +190,40 @@ cudaError_t dispatch_policy(int task, const mrsim_dev::PolicyParams<Real>& p, cu
 }
 
 template <class Real>
+cudaError_t dispatch_scripted(int task, const mrsim_dev::ScriptedParams<Real>& p, cudaStream_t s) {
+    using namespace mrsim_host;
+    switch (task) {
+        case 0: return launch_scripted<Real, 0>(p, s);
+        case 1: return launch_scripted<Real, 1>(p, s);
+        case 2: return launch_scripted<Real, 2>(p, s);
+        case 3: return launch_scripted<Real, 3>(p, s);
+        case 4: return launch_scripted<Real, 4>(p, s);
+        case 5: return launch_scripted<Real, 5>(p, s);
+        case 6: return launch_scripted<Real, 6>(p, s);
+        case 7: return launch_scripted<Real, 7>(p, s);
+        default: return launch_scripted<Real, 8>(p, s);
+    }
+}
+
+template <class Real>
+cudaError_t scripted_launch(mrsim_ctx* ctx, const DevState<Real>& st, int8_t* out, cudaStream_t s) {
+    mrsim_dev::ScriptedParams<Real> p;
+    std::memset(&p, 0, sizeof p);
+    p.c = ctx->cfg;
+    p.s = st;
+    p.B = ctx->B;
+    p.N = ctx->N;
+    p.nf = ctx->nf;
+    p.ni = ctx->ni;
+    p.kind = ctx->scripted;
+    mrsim_dev::prey_offsets(ctx->cfg, p.prey_off);
+    p.actions = out;
+    return dispatch_scripted<Real>(ctx->cfg.task, p, s);
+}
+
+template <class Real>
 cudaError_t policy_launch(mrsim_ctx* ctx, const DevState<Real>& st, int8_t* out, cudaStream_t s) {
+    if (ctx->scripted) return scripted_launch<Real>(ctx, st, out, s);
     mrsim_dev::PolicyParams<Real> p;
     p.c = ctx->cfg;
     p.s = st;
@@ -646,8 +680,9 @@ int capture_step(mrsim_ctx* ctx, const int8_t* actions, float* obs, float* rewar
     if (!ctx->d_done) CK(cudaMalloc(&ctx->d_done, ctx->B));
     if (!actions) {
         if (!ctx->d_pol_actions) CK(cudaMalloc(&ctx->d_pol_actions, BN));
-        int rc = ctx->ff ? run_policy(ctx, ctx->d_pol_actions, s) : MRSIM_OK;
-        if (!ctx->ff) {
+        const bool dev_policy = ctx->ff || ctx->scripted;
+        int rc = dev_policy ? run_policy(ctx, ctx->d_pol_actions, s) : MRSIM_OK;
+        if (!dev_policy) {
             const unsigned grid = static_cast<unsigned>((BN + 255) / 256);
             if (ctx->fp64)
                 mrsim_dev::random_actions_kernel<double><<<grid, 256, 0, s>>>(
@@ -839,7 +874,7 @@ int mrsim_step(mrsim_ctx* ctx, const int8_t* actions_dev, float* obs_dev, float*
         return set_err(ctx, MRSIM_E_INVALID_ARGUMENT, "auto-reset needs mrsim_reset_episodes (episode seeds)");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (ctx->d_cap) return capture_step(ctx, actions_dev, obs_dev, reward_dev, done_dev, next_obs_dev, s);
-    if (!actions_dev && ctx->ff) {  // the producer before the step: the feedforward policy on device
+    if (!actions_dev && (ctx->ff || ctx->scripted)) {  // the producer before the step: the policy on device
         CK(cudaSetDevice(ctx->device));
         const int rc = run_policy(ctx, ctx->d_pol_actions, s);
         if (rc != MRSIM_OK) return rc;
@@ -928,6 +963,25 @@ int mrsim_observe_host(mrsim_ctx* ctx, float* obs_host) {
 int mrsim_set_policy_random(mrsim_ctx* ctx) {
     if (!ctx) return MRSIM_E_INVALID_ARGUMENT;
     ctx->ff = false;
+    ctx->scripted = 0;
+    return MRSIM_OK;
+}
+
+int mrsim_set_policy_scripted(mrsim_ctx* ctx, int kind) {
+    if (!ctx) return MRSIM_E_INVALID_ARGUMENT;
+    if (kind != MRSIM_POLICY_SCRIPTED_GOAL && kind != MRSIM_POLICY_PREY_CHASER)
+        return set_err(ctx, MRSIM_E_INVALID_ARGUMENT, "unknown scripted policy");
+    if (kind == MRSIM_POLICY_PREY_CHASER && ctx->cfg.task != MRSIM_TASK_PREDATOR_PREY)
+        return set_err(ctx, MRSIM_E_INVALID_ARGUMENT, "prey_chaser policy only applies to predator_prey");
+    const double cell = 0.05;  // policy.hpp:253-255
+    const int cols = static_cast<int>((2.0 * ctx->cfg.arena_half_width) / cell);
+    const int rows = static_cast<int>((2.0 * ctx->cfg.arena_half_height) / cell);
+    if (cols * rows > mrsim_dev::kGridMaxCells)
+        return set_err(ctx, MRSIM_E_UNSUPPORTED, "scripted planner grid exceeds the device capacity");
+    CK(cudaSetDevice(ctx->device));
+    if (!ctx->d_pol_actions) CK(cudaMalloc(&ctx->d_pol_actions, ctx->B * ctx->N));
+    ctx->ff = false;
+    ctx->scripted = kind;
     return MRSIM_OK;
 }
 
@@ -988,12 +1042,13 @@ int mrsim_set_policy_feedforward(mrsim_ctx* ctx, int num_layers, const int32_t* 
     if (!ctx->d_pol_actions) CK(cudaMalloc(&ctx->d_pol_actions, ctx->B * ctx->N));
     ctx->net = net;
     ctx->ff = true;
+    ctx->scripted = 0;
     return MRSIM_OK;
 }
 
 int mrsim_policy_actions(mrsim_ctx* ctx, int8_t* actions_dev, void* stream) {
     if (!ctx || !actions_dev) return MRSIM_E_INVALID_ARGUMENT;
-    if (!ctx->ff) return mrsim_random_actions(ctx, actions_dev, stream);
+    if (!ctx->ff && !ctx->scripted) return mrsim_random_actions(ctx, actions_dev, stream);
     CK(cudaSetDevice(ctx->device));
     return run_policy(ctx, actions_dev, static_cast<cudaStream_t>(stream));
 }

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include "policy.cuh"
+#include "scripted.cuh"
 #include "step_kernel.cuh"
 
 namespace mrsim_host {
@@ -71,5 +72,7 @@ template <class Real, int TASK>
 cudaError_t launch_reset(const mrsim_dev::ResetParams<Real>& p, cudaStream_t stream);
 template <class Real, int TASK>
 cudaError_t launch_policy(const mrsim_dev::PolicyParams<Real>& p, cudaStream_t stream);
+template <class Real, int TASK>
+cudaError_t launch_scripted(const mrsim_dev::ScriptedParams<Real>& p, cudaStream_t stream);
 
 }  // namespace mrsim_host

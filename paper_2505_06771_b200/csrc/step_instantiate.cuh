@@ -127,4 +127,26 @@ cudaError_t launch_policy<double, MRSIM_TASK_ID>(const mrsim_dev::PolicyParams<d
     return launch_policy_any<double>(p, s);
 }
 
+template <class Real>
+static cudaError_t launch_scripted_any(const mrsim_dev::ScriptedParams<Real>& p, cudaStream_t s) {
+    const long long want = (p.B + mrsim_dev::kPolicyWarps - 1) / mrsim_dev::kPolicyWarps;
+    const unsigned grid = static_cast<unsigned>(want < 148 * 16 ? want : 148 * 16);
+    const int smem = static_cast<int>(sizeof(mrsim_dev::ScriptedSmem)) * mrsim_dev::kPolicyWarps;
+    auto k = mrsim_dev::scripted_kernel<Real, MRSIM_TASK_ID>;
+    if (smem > 48 * 1024) {
+        const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+    }
+    k<<<grid, 32 * mrsim_dev::kPolicyWarps, smem, s>>>(p);
+    return cudaGetLastError();
+}
+template <>
+cudaError_t launch_scripted<float, MRSIM_TASK_ID>(const mrsim_dev::ScriptedParams<float>& p, cudaStream_t s) {
+    return launch_scripted_any<float>(p, s);
+}
+template <>
+cudaError_t launch_scripted<double, MRSIM_TASK_ID>(const mrsim_dev::ScriptedParams<double>& p, cudaStream_t s) {
+    return launch_scripted_any<double>(p, s);
+}
+
 }  // namespace mrsim_host

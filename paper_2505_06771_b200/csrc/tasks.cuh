@@ -318,6 +318,33 @@ __device__ __forceinline__ Real step_size_of(const mrsim_cfg& c, const int* ti, 
     return Real(c.step_sizes[i]);
 }
 
+// prey_heuristic (predator_prey.hpp:15-34): of the prey's 9 candidate moves (stay, then E, NE,
+// N, ... scaled by prey_step; offsets precomputed on the host with the reference's libm) inside
+// the arena, the one farthest from the nearest robot; strict `>`, so the first index wins ties.
+template <class Real>
+__device__ __forceinline__ void prey_heuristic_dev(const mrsim_cfg& c, const double* prey_off, Real px, Real py,
+                                                   const Real* xs, const Real* ys, int N, Real& bx, Real& by) {
+    const Real hw = Real(c.arena_half_width), hh = Real(c.arena_half_height);
+    bx = px;
+    by = py;
+    Real best = -Consts<Real>::inf;
+    for (int k = 0; k < 9; ++k) {
+        Real cx = px, cy = py;
+        if (k > 0) {
+            cx = px + Real(prey_off[2 * (k - 1)]);
+            cy = py + Real(prey_off[2 * (k - 1) + 1]);
+        }
+        if (!(cx >= -hw && cx <= hw && cy >= -hh && cy <= hh)) continue;
+        Real nearest = Consts<Real>::inf;
+        for (int i = 0; i < N; ++i) nearest = dmin(nearest, dhypot(cx - xs[i], cy - ys[i]));
+        if (nearest > best) {
+            best = nearest;
+            bx = cx;
+            by = cy;
+        }
+    }
+}
+
 // Scenario::transition + Scenario::finalize, run by one lane on the staged
 // state after the physics ticks. Returns the team reward (before the
 // collision violation term, which the engine adds: batch.hpp:213-217).
@@ -330,25 +357,8 @@ __device__ Real transition_task(const mrsim_cfg& c, EnvView<Real>& v, Rng& rng, 
         for (int i = 0; i < N; ++i) total += dhypot(v.xs[i] - v.tf[2 * i], v.ys[i] - v.tf[2 * i + 1]);
         return Real(c.coef[MRSIM_COEF_DIST]) * total;
     } else if (TASK == MRSIM_TASK_PREDATOR_PREY) {  // predator_prey.hpp:121-143, 183-199
-        const Real hw = Real(c.arena_half_width), hh = Real(c.arena_half_height);
-        const Real px = v.tf[0], py = v.tf[1];
-        Real bx = px, by = py;
-        Real best = -Consts<Real>::inf;
-        for (int k = 0; k < 9; ++k) {
-            Real cx = px, cy = py;
-            if (k > 0) {  // candidate offsets cos/sin((k-1) pi/4) * prey_step, precomputed on the host
-                cx = px + Real(v.prey_off[2 * (k - 1)]);
-                cy = py + Real(v.prey_off[2 * (k - 1) + 1]);
-            }
-            if (!(cx >= -hw && cx <= hw && cy >= -hh && cy <= hh)) continue;
-            Real nearest = Consts<Real>::inf;
-            for (int i = 0; i < N; ++i) nearest = dmin(nearest, dhypot(cx - v.xs[i], cy - v.ys[i]));
-            if (nearest > best) {
-                best = nearest;
-                bx = cx;
-                by = cy;
-            }
-        }
+        Real bx, by;
+        prey_heuristic_dev<Real>(c, v.prey_off, v.tf[0], v.tf[1], v.xs, v.ys, N, bx, by);
         v.tf[0] = bx;
         v.tf[1] = by;
         bool tagged = false;

@@ -128,8 +128,10 @@ def parse_policy(text: str) -> tuple[str, str, bool]:
             if not text[len(prefix):]:
                 raise InvalidArgument("feedforward policy needs a weights file path")
             return "feedforward", text[len(prefix):], greedy
-    if text in ("scripted_goal", "scripted", "prey_chaser"):
-        raise InvalidArgument(f"policy '{text}' is a host-side scripted policy (not on the device path)")
+    if text in ("scripted_goal", "scripted"):
+        return "scripted_goal", "", True
+    if text == "prey_chaser":
+        return "prey_chaser", "", True
     raise InvalidArgument(f"unknown policy '{text}'")
 
 
@@ -171,7 +173,8 @@ def build_header(run: RunConfig, cfg: ScenarioConfig) -> TrajectoryHeader:
     h.set("barriers", "1" if cfg.raw.barrier_enabled else "0")
     h.set("noise_scale", format_double(cfg.raw.action_noise_scale))
     kind, path, greedy = parse_policy(run.policy)
-    h.set("policy", "random" if kind == "random" else ("feedforward:" if greedy else "feedforward_sample:") + path)
+    h.set("policy", kind if kind in ("random", "scripted_goal", "prey_chaser")
+          else ("feedforward:" if greedy else "feedforward_sample:") + path)
     defaults = make_default_config(run.scenario)
     for key in sorted(run.layout_overrides):
         vals = [float(v) for v in run.layout_overrides[key]]
@@ -226,7 +229,7 @@ def run_episodes(run: RunConfig, out: str | None = None, device: int = 0, max_wa
     for wave_start in range(0, run.episodes, wave_size):
         wave = min(wave_size, run.episodes - wave_start)
         gb = CudaEnvBatch(cfg, wave, device=device, fp64=True)
-        if kind == "feedforward":
+        if kind != "random":
             gb.set_policy(run.policy)
         gb.reset_episodes(root_seed=run.seed, first_episode=wave_start, episode_stride=wave)
         gb._check(lib().mrsim_capture_begin(gb._h, T))

@@ -111,3 +111,53 @@ def test_policy_validation_errors():
     gb.set_policy("random")  # back to the harness random policy
     a = gb.policy_actions().cpu().numpy()
     assert a.shape == (4, 3) and a.min() >= 0 and a.max() <= 4
+
+
+SCRIPTED = [("navigation", 4), ("predator_prey", 6), ("discovery", 6), ("rware", 4), ("foraging", 4),
+            ("material_transport", 10), ("arctic_transport", 10), ("warehouse", 4), ("random_waypoints", 4)]
+
+
+@pytest.mark.parametrize("task,n", SCRIPTED)
+def test_scripted_goal_policy_matches_reference(task, n, ref):
+    """PolicyKind::ScriptedGoal (policy.hpp:242-360): BFS planner on the device.
+    Near-ties (device hypot vs glibc, <= 1 ulp) may flip a decision: <= 1 in 500."""
+    cfg, sp = make_cfgs(ref, task, n)
+    B = 48
+    seeds = [m.derive_episode_seed(21, e) for e in range(B)]
+    rb = ref.RefBatch(sp)
+    rb.reset(seeds)
+    gb = m.CudaEnvBatch(cfg, B, fp64=True)
+    gb.reset_seeds(seeds)
+    gb.set_policy("scripted_goal")
+    flips = total = 0
+    for t in range(12):
+        ra = rb.policy_actions("scripted_goal")
+        ga = gb.policy_actions().cpu().numpy().astype(np.int32)
+        flips += int(np.sum(ga != ra))
+        total += ga.size
+        gb.step_host(ra)
+        rb.step(ra)
+    assert flips <= max(1, total // 500), (flips, total)
+
+
+def test_prey_chaser_policy_matches_reference(ref):
+    cfg, sp = make_cfgs(ref, "predator_prey", 6)
+    B = 64
+    seeds = [m.derive_episode_seed(22, e) for e in range(B)]
+    rb = ref.RefBatch(sp)
+    rb.reset(seeds)
+    gb = m.CudaEnvBatch(cfg, B, fp64=True)
+    gb.reset_seeds(seeds)
+    gb.set_policy("prey_chaser")
+    flips = total = 0
+    for t in range(30):
+        ra = rb.policy_actions("prey_chaser")
+        ga = gb.policy_actions().cpu().numpy().astype(np.int32)
+        flips += int(np.sum(ga != ra))
+        total += ga.size
+        gb.step_host(ra)
+        rb.step(ra)
+    assert flips <= max(1, total // 500), (flips, total)
+    nav = m.CudaEnvBatch(m.make_default_config("navigation"), 2)
+    with pytest.raises(m.InvalidArgument, match="prey_chaser policy only applies to predator_prey"):
+        nav.set_policy("prey_chaser")
