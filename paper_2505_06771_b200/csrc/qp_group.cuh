@@ -44,8 +44,9 @@ struct QpWs {
     Real *S, *lam, *r, *d;
     Desc* desc;
     int* act;
+    int* warm;  // the group's previous active rows, in logical order (warm-started entering order)
     static __host__ __device__ constexpr int bytes(int n) {
-        return static_cast<int>(sizeof(Real)) * (n * n + 3 * n) + static_cast<int>(sizeof(Desc)) * n + 4 * n;
+        return static_cast<int>(sizeof(Real)) * (n * n + 3 * n) + static_cast<int>(sizeof(Desc)) * n + 8 * n;
     }
     __device__ void carve(unsigned char* base, int n) {
         S = reinterpret_cast<Real*>(base);
@@ -54,6 +55,7 @@ struct QpWs {
         d = r + n;
         desc = reinterpret_cast<Desc*>(d + n);
         act = reinterpret_cast<int*>(desc + n);
+        warm = act + n;
     }
 };
 
@@ -62,9 +64,20 @@ struct QpWs {
 // FAST: specialise the first entering row when the whole warp starts from an
 // empty active set (same arithmetic; a speed/register-pressure trade chosen
 // per task, see qp_fast_first_row in step_kernel.cuh).
+//
+// Warm entering order (warm_k != nullptr): the rows active at the end of the
+// group's previous solve (ws.warm, *warm_k of them, rebuilt on this tick's
+// geometry) are offered as the entering rows of the first iterations, in
+// their previous order, instead of the most violated row of a scan; a row no
+// longer violated is passed over (the inner loop leaves u unchanged). The
+// iteration is otherwise the method above, so it reaches the same unique
+// optimum (strictly convex QP): only the internal path, and so rounding at
+// the 1e-16 level, differs from the cold most-violated-first order. A warp
+// skips its row scan while every group still has a warm row to offer.
 template <class Real, int L, bool FAST = true, class RowSet>
 __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpWs<Real, typename RowSet::Desc>& ws,
-                                        int n, bool participate, Real& ux, Real& uy, int total_rows, Real tol) {
+                                        int n, bool participate, Real& ux, Real& uy, int total_rows, Real tol,
+                                        int* warm_k = nullptr) {
     typedef typename RowSet::Desc Desc;
     const int lane = g.lane;
     const bool vl = 2 * lane < n;      // this lane's x variable exists
@@ -78,16 +91,22 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
     bool done = !participate;
     int iter = 0;
     const int max_iterations = 100 + 20 * total_rows;  // qp.hpp:193
+    const int wk = (warm_k && participate) ? *warm_k : 0;  // warm rows on offer (group-uniform)
+    int wi = 0;
     while (Grp<L>::warp_any(!done)) {
         if (!done && iter >= max_iterations) {
             status = kQpIterLimit;
             done = true;
         }
-        // Most violated inactive row (qp.hpp:225-239).
+        // Most violated inactive row (qp.hpp:225-239), or the next warm row.
         Real worst = tol;
         int p = -1;
-        rows.scan(g, ux, uy, worst, p);
-        g.argmax(worst, p);
+        const bool forced = !done && wi < wk;
+        if (Grp<L>::warp_any(!done && !forced)) {
+            rows.scan(g, ux, uy, worst, p);
+            g.argmax(worst, p);
+        }
+        if (forced) p = ws.warm[wi++];
         if (!done && p < 0) done = true;
         if (!Grp<L>::warp_any(!done)) break;  // every env of the warp is optimal
         bool act = !done;
@@ -305,8 +324,14 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
             if (in && guard > total_rows) in = false;  // guard exhausted without adding
             Grp<L>::sync();
         }
-        if (act && !added) done = true;  // stall (qp.hpp:331-334) or infeasible
+        if (act && !added && !forced) done = true;  // stall (qp.hpp:331-334) or infeasible
         if (act) ++iter;
+    }
+    if (warm_k) {  // remember this solve's active rows, in logical order
+        if (participate && lp0 >= 0) ws.warm[lp0] = ws.act[q0];
+        if (participate && lp1 >= 0) ws.warm[lp1] = ws.act[q1];
+        *warm_k = (participate && status == kQpOptimal) ? k : 0;
+        Grp<L>::sync();
     }
     return status;
 }

@@ -330,7 +330,7 @@ template <class Real, int L, int MP, int MO, bool FAST>
 __device__ __forceinline__ int barrier_filter(const Grp<L>& g, BarrierRows<Real, L, MP, MO>& rows,
                                               const QpWs<Real, BarrierDesc<Real>>& ws,
                               const PhysConsts<Real>& k, bool participate, Real prx, Real pry, Real cs, Real sn,
-                              Real nv, Real nw, int total_rows, Real& cv, Real& cw) {
+                              Real nv, Real nw, int total_rows, Real& cv, Real& cw, int* warm_k = nullptr) {
     const int lane = g.lane;
     const int n = 2 * rows.N;
     // u_nom = uni_to_si(clamped nominal) (controllers.hpp:59-65)
@@ -386,7 +386,7 @@ __device__ __forceinline__ int barrier_filter(const Grp<L>& g, BarrierRows<Real,
     const bool bad = g.any(coincident);  // (the ballot also orders the row-cache writes before the QP reads)
     Grp<L>::sync();
     rows.active = 0;
-    const int status = qp_solve<Real, L, FAST>(g, rows, ws, n, participate && !bad, ux, uy, total_rows, k.tol);
+    const int status = qp_solve<Real, L, FAST>(g, rows, ws, n, participate && !bad, ux, uy, total_rows, k.tol, warm_k);
     // map back + uniform scale (barrier.hpp:186-204)
     const Real mv = cs * ux + sn * uy;
     const Real mw = (-sn * ux + cs * uy) * k.inv_l;
@@ -447,6 +447,18 @@ __device__ __forceinline__ Real wrap_angle_dev(Real t) {
 // The fused step kernel. Persistent grid-stride loop; each warp steps 32/L
 // environments in lockstep (ghost groups past the end compute but never store).
 // ---------------------------------------------------------------------------
+// Offer the previous tick's active rows first (qp_solve warm entering order): a
+// measured per-task choice (B200, fp64). It pays where the active set is large
+// and stable (arctic_transport N=10, ~7 active rows per tick: +11 %); where
+// most ticks enter 0-2 rows the offered rows are often slack again and the
+// extra iterations cost 1-8 % (navigation ... material_transport).
+#ifndef MRSIM_QP_WARM
+#define MRSIM_QP_WARM 1
+#endif
+__host__ __device__ constexpr bool qp_warm_order(int task) {
+    return MRSIM_QP_WARM != 0 && task == MRSIM_TASK_ARCTIC_TRANSPORT;
+}
+
 // First-row QP fast path (qp_solve FAST): a measured choice (B200, fp64). It
 // pays for groups of 4 (teams of up to 4 robots: navigation +6%, warehouse +7%,
 // foraging +4%, rware neutral) and costs 2-4% for L = 8 (discovery / foraging
@@ -586,6 +598,7 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
         Real min_d2 = Consts<Real>::inf;  // min squared pairwise distance over this step's ticks
         int qp_inf = p.in.qp_inf[e];
         bool collision = false;
+        int warm_k = 0;  // QP warm entering order: the previous tick's active rows (none at a step's first tick)
         for (int tick = 0; tick < c.sub_steps; ++tick) {
             Real sn, cs;
             dsincos(th, &sn, &cs);
@@ -618,7 +631,7 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
             Real cv = nv, cw = nw;
             if (c.barrier_enabled) {
                 const int bs = barrier_filter<Real, L, MP, MO, qp_fast_first_row(L)>(g, rows, sm.qp, p.k, !skip, prx, pry, cs, sn, nv, nw,
-                                                       total_rows, cv, cw);
+                                                       total_rows, cv, cw, qp_warm_order(TASK) ? &warm_k : nullptr);
                 if (bs < 0 && !skip) {
                     if (lane == 0) {
                         report_error(p.err, e, 0, kErrCoincident);
