@@ -47,11 +47,9 @@ struct mrsim_ctx {
     int smem_group = 0;
     int obs_stage = 0;  // floats per warp of the staged obs store (0: direct stores)
     // host-API scratch
-    int8_t* d_actions = nullptr;
     float* d_obs = nullptr;
     double* d_reward64 = nullptr;
     uint8_t* d_done = nullptr;
-    int8_t* h_actions = nullptr;  // pinned (unused since the int32 upload)
     unsigned long long* h_err = nullptr;  // pinned copy of the device error word + serial
     int32_t* d_actions32 = nullptr;
     bool reset_done = false;
@@ -816,12 +814,10 @@ void mrsim_destroy(mrsim_ctx* ctx) {
     for (int k = 0; k < 2; ++k) cudaFree(ctx->mem[k]);
     cudaFree(ctx->stats_mem);
     cudaFree(ctx->d_err);
-    cudaFree(ctx->d_actions);
     cudaFree(ctx->d_actions32);
     cudaFree(ctx->d_obs);
     cudaFree(ctx->d_reward64);
     cudaFree(ctx->d_done);
-    if (ctx->h_actions) cudaFreeHost(ctx->h_actions);
     if (ctx->h_err) cudaFreeHost(ctx->h_err);
     cudaFree(ctx->d_wT);
     cudaFree(ctx->d_bias);
