@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--dist-backend", default="nccl", help="nccl (GPUs) or gloo (multi-rank smoke test)")
     ap.add_argument("--controller", default="unicycle_position", choices=["unicycle_position", "unicycle_pose"],
                     help="ControllerKind (framework.hpp:126)")
+    ap.add_argument("--policy", default="random", choices=["random", "mlp", "scripted_goal", "prey_chaser"],
+                    help="on-device policy producing each step's actions (mlp: a random 64-32 relu network)")
     return ap.parse_args()
 
 
@@ -71,7 +73,8 @@ def dist_env():
 
 def workload_name(a) -> str:
     ctl = "" if a.controller == "unicycle_position" else ", pose controller"
-    acts = "stored random waypoints" if a.task == "random_waypoints" else "random actions"
+    acts = "stored random waypoints" if a.task == "random_waypoints" else (
+        "random actions" if a.policy == "random" else f"on-device {a.policy} policy")
     return f"{a.task} N={a.robots}, {a.envs} envs/GPU, {a.max_steps}-step episodes, CBF on{ctl}, {acts}"
 
 
@@ -202,6 +205,11 @@ def main():
     B = a.envs
     batch = m.CudaEnvBatch(cfg, B, device=local, fp64=(not a.fp32), auto_reset=True)
     batch.reset_episodes(root_seed=0, first_episode=rank * B, episode_stride=world * B)
+    if a.policy == "mlp":
+        batch.set_policy(m.FeedforwardWeights.random([cfg.obs_dim, 64, 32, 5], ["relu", "relu", "identity"], seed=1))
+    elif a.policy != "random":
+        batch.set_policy(a.policy)
+    launches_per_step = 1 if a.policy == "random" else 2  # the policy kernel, then the step
     stream = torch.cuda.current_stream()
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
@@ -323,7 +331,7 @@ def main():
                                   "peak_source": "measured FMA-chain probe (mrsim_probe_fma_peak) on this GPU"}},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": a.steps,
+            "gpu_launches": a.steps * launches_per_step,
             "clocks": clk,
             "wall_s_timed_region": wall,
             "episodes": {"completed": float(red[0].item()),

@@ -28,6 +28,7 @@ struct ScriptedSmem {
     int ti[kTiMax];
     int drones[MRSIM_MAX_ROBOTS];
     unsigned blocked[kGridWords], frontier[kGridWords], visited[kGridWords], next[kGridWords];
+    unsigned colE[kGridWords], colW[kGridWords];  // cells that have an east / west neighbour column
     unsigned short dist[kGridMaxCells];  // BFS level + 1 (0 = unreached)
 };
 
@@ -243,8 +244,14 @@ __device__ int scripted_goal_action_dev(const mrsim_cfg& c, ScriptedSmem& s, int
                 b = dist2d(p.x, p.y, s.xs[j], s.ys[j]) < robot_clear;
             }
         }
-        const unsigned word = __ballot_sync(0xffffffffu, b);
-        if (lane == 0) s.blocked[w] = word;
+        const unsigned word = __ballot_sync(0xffffffffu, b || idx >= ncell);  // bits past the grid: never free
+        const unsigned east = __ballot_sync(0xffffffffu, idx < ncell && idx % cols != cols - 1);
+        const unsigned west = __ballot_sync(0xffffffffu, idx < ncell && idx % cols != 0);
+        if (lane == 0) {
+            s.blocked[w] = word;
+            s.colE[w] = east;
+            s.colW[w] = west;
+        }
     }
     __syncwarp();
     int sc, sr, gc, gr;
@@ -285,29 +292,29 @@ __device__ int scripted_goal_action_dev(const mrsim_cfg& c, ScriptedSmem& s, int
     }
     for (int idx = lane; idx < ncell; idx += 32) s.dist[idx] = (idx == g0) ? 1 : 0;
     __syncwarp();
-    auto bit = [&](const unsigned* bs, int i) -> unsigned {  // bit i of a bitset, 0 outside [0, ncell)
-        return (i >= 0 && i < ncell) ? ((bs[i >> 5] >> (i & 31)) & 1u) : 0u;
+    // 32 bits of a bitset starting at bit `start` (may lie outside the grid: those bits read as 0)
+    auto window = [&](const unsigned* bs, int start) -> unsigned {
+        const int wq = start >= 0 ? (start >> 5) : -((31 - start) >> 5);
+        const int sh = start - wq * 32;
+        const unsigned lo = (wq >= 0 && wq < nw) ? bs[wq] : 0u;
+        const unsigned hi = (wq + 1 >= 0 && wq + 1 < nw) ? bs[wq + 1] : 0u;
+        return sh ? ((lo >> sh) | (hi << (32 - sh))) : lo;
     };
     for (int level = 1; level < ncell; ++level) {
+        // a free, unvisited cell joins this level if any of its 8 neighbours is in the frontier
         bool any = false;
         for (int w = lane; w < nw; w += 32) {
-            unsigned word = 0;
-            for (int b = 0; b < 32; ++b) {
-                const int i = w * 32 + b;
-                if (i >= ncell) break;
-                if (bit(s.visited, i) || bit(s.blocked, i)) continue;
-                const int cc = i % cols, rr = i / cols;
-                bool hit = false;
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const int dc = (k == 0 || k == 4 || k == 5) ? 1 : ((k == 1 || k == 6 || k == 7) ? -1 : 0);
-                    const int dr = (k == 2 || k == 4 || k == 6) ? 1 : ((k == 3 || k == 5 || k == 7) ? -1 : 0);
-                    const int nc = cc + dc, nr = rr + dr;
-                    if (nc < 0 || nr < 0 || nc >= cols || nr >= rows) continue;
-                    hit = hit || bit(s.frontier, nr * cols + nc);
-                }
-                if (hit) word |= 1u << b;
-            }
+            const int base = w * 32;
+            unsigned hit = 0u;
+            hit |= window(s.frontier, base + 1) & s.colE[w];             // (+1, 0)
+            hit |= window(s.frontier, base - 1) & s.colW[w];             // (-1, 0)
+            hit |= window(s.frontier, base + cols);                      // (0, +1)
+            hit |= window(s.frontier, base - cols);                      // (0, -1)
+            hit |= window(s.frontier, base + cols + 1) & s.colE[w];      // (+1, +1)
+            hit |= window(s.frontier, base - cols + 1) & s.colE[w];      // (+1, -1)
+            hit |= window(s.frontier, base + cols - 1) & s.colW[w];      // (-1, +1)
+            hit |= window(s.frontier, base - cols - 1) & s.colW[w];      // (-1, -1)
+            const unsigned word = hit & ~s.visited[w] & ~s.blocked[w];
             s.next[w] = word;
             any = any || word != 0u;
         }
@@ -396,11 +403,13 @@ __global__ void __launch_bounds__(32 * kPolicyWarps) scripted_kernel(const __gri
         for (int f = lane; f < p.nf; f += 32) sm.tf[f] = double(p.s.tf[static_cast<long long>(f) * p.B + e]);
         for (int w = lane; w < p.ni; w += 32) sm.ti[w] = p.s.ti[static_cast<long long>(w) * p.B + e];
         __syncwarp();
+        if (TASK == MRSIM_TASK_PREDATOR_PREY && p.kind == MRSIM_POLICY_PREY_CHASER) {
+            if (lane < N) p.actions[e * N + lane] = static_cast<int8_t>(prey_chaser_dev(c, sm, p.prey_off, lane, travel));
+            continue;  // (the loop head syncs the warp before the next env is staged)
+        }
         for (int r = 0; r < N; ++r) {
             int a;
-            if (TASK == MRSIM_TASK_PREDATOR_PREY && p.kind == MRSIM_POLICY_PREY_CHASER) {
-                a = prey_chaser_dev(c, sm, p.prey_off, r, travel);
-            } else {
+            {
                 const double step = double(step_size_of<TASK, double>(c, sm.ti, r, sm.xs[r], sm.ys[r]));
                 a = scripted_goal_action_dev<TASK>(c, sm, r, step, travel);
             }
