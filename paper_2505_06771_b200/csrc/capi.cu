@@ -234,6 +234,10 @@ cudaError_t policy_launch(mrsim_ctx* ctx, const DevState<Real>& st, int8_t* out,
     p.wT = ctx->d_wT;
     p.bias = ctx->d_bias;
     p.net = ctx->net;
+    int maxw = ctx->D;
+    for (int l = 0; l < ctx->net.num_layers; ++l) maxw = maxw > ctx->net.out[l] ? maxw : ctx->net.out[l];
+    p.maxw = maxw;
+    p.warp_bytes = mrsim_dev::policy_warp_bytes<Real>(ctx->N, maxw);
     p.actions = out;
     return dispatch_policy<Real>(ctx->cfg.task, p, s);
 }

@@ -3,12 +3,13 @@
 // FeedforwardWeights::forward, policy.hpp:95-116; harness.hpp:238-252).
 //
 // One warp per environment. The warp stages the env's state in shared
-// memory, then per robot: assembles the observation (the same features the
-// step kernel stores, unrounded, in the state precision), runs the dense
-// layers with lanes splitting the output neurons (weights stored transposed
-// [in][out] so a warp's loads of one input row are contiguous), and lane 0
-// picks the action: greedy argmax (strict `>`, first maximum wins) or a
-// softmax sample from policy_stream(episode seed, step, robot).
+// memory, assembles every robot's observation (the same features the step
+// kernel stores, unrounded, in the state precision), runs the dense layers
+// for all robots at once with lanes owning (robot, neuron) outputs, four
+// independent accumulation chains per lane (weights stored transposed
+// [in][out], read through L1), and lane r picks robot r's action: greedy
+// argmax (strict `>`, first maximum wins) or a softmax sample from
+// policy_stream(episode seed, step, robot).
 //
 // Arithmetic: each neuron is b + w0*x0 + w1*x1 + ... accumulated in input
 // order with explicitly rounded multiply and add (no FMA contraction), the
@@ -38,32 +39,39 @@ struct PolicyParams {
     DevState<Real> s;
     long long B;
     int N, D, bdim, nf, ni;
+    int maxw;          // max(D, layer widths): row stride of the activation buffers
+    int warp_bytes;    // dynamic shared memory per warp
     const double* wT;  // per layer [in][out]
     const double* bias;
     PolicyNet net;
     int8_t* actions;   // [B][N]
 };
 
-// Per-warp shared memory: state staging + two activation buffers.
+// Per-warp shared memory: state staging, then two activation buffers [N][maxw] (dynamic).
 template <class Real>
-struct PolicySmem {
+struct PolicyStage {
     Real xs[MRSIM_MAX_ROBOTS], ys[MRSIM_MAX_ROBOTS], ts[MRSIM_MAX_ROBOTS], tf[kTfMax];
     int ti[kTiMax];
     int drones[MRSIM_MAX_ROBOTS];
-    double h[2][kPolicyMaxWidth];
 };
+template <class Real>
+__host__ __device__ constexpr int policy_warp_bytes(int N, int maxw) {
+    return ((static_cast<int>(sizeof(PolicyStage<Real>)) + 15) & ~15) + 2 * N * maxw * 8;
+}
 
 template <class Real, int TASK>
 __global__ void __launch_bounds__(32 * kPolicyWarps) policy_kernel(const __grid_constant__ PolicyParams<Real> p) {
-    __shared__ PolicySmem<Real> smem[kPolicyWarps];
+    extern __shared__ __align__(16) unsigned char pol_smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    PolicySmem<Real>& sm = smem[wib];
+    unsigned char* base = pol_smem + wib * p.warp_bytes;
+    PolicyStage<Real>& sm = *reinterpret_cast<PolicyStage<Real>*>(base);
+    double* bufs = reinterpret_cast<double*>(base + ((static_cast<int>(sizeof(PolicyStage<Real>)) + 15) & ~15));
     const mrsim_cfg& c = p.c;
-    const int N = p.N;
+    const int N = p.N, W = p.maxw;
     if (lane == 0) arctic_drones(c, sm.drones);
     const EnvView<Real> view{sm.xs, sm.ys, sm.ts, sm.tf, sm.ti, N, sm.drones, nullptr};
-    const long long stride = static_cast<long long>(gridDim.x) * kPolicyWarps;
-    for (long long e = static_cast<long long>(blockIdx.x) * kPolicyWarps + wib; e < p.B; e += stride) {
+    const long long stride = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
+    for (long long e = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + wib; e < p.B; e += stride) {
         __syncwarp();
         if (lane < N) {
             sm.xs[lane] = p.s.px[e * N + lane];
@@ -75,55 +83,77 @@ __global__ void __launch_bounds__(32 * kPolicyWarps) policy_kernel(const __grid_
         const int step = p.s.step_index[e];
         const uint64_t pkey = p.s.pkey[e];
         __syncwarp();
-        for (int r = 0; r < N; ++r) {
-            // observation of robot r (assemble_observations, batch.hpp:143-151)
-            for (int q = lane; q < p.D; q += 32) sm.h[0][q] = double(obs_feature<TASK, Real>(c, view, r, q, p.bdim));
-            __syncwarp();
-            int cur = 0;
-            for (int l = 0; l < p.net.num_layers; ++l) {  // FeedforwardWeights::forward (policy.hpp:95-116)
-                const int nin = p.net.in[l], nout = p.net.out[l], act = p.net.act[l];
-                const double* W = p.wT + p.net.w_off[l];
-                const double* bb = p.bias + p.net.b_off[l];
-                const double* x = sm.h[cur];
-                double* y = sm.h[cur ^ 1];
-                for (int o = lane; o < nout; o += 32) {
-                    double acc = __ldg(bb + o);
-                    for (int i = 0; i < nin; ++i) acc = __dadd_rn(acc, __dmul_rn(__ldg(W + static_cast<long long>(i) * nout + o), x[i]));
-                    if (act == MRSIM_ACT_RELU) acc = acc > 0 ? acc : 0.0;
-                    else if (act == MRSIM_ACT_TANH) acc = tanh(acc);
-                    y[o] = acc;
+        // every robot's observation (assemble_observations, batch.hpp:143-151), unrounded
+        double* x = bufs;
+        double* y = bufs + N * W;
+        for (int q = lane; q < N * p.D; q += 32) {
+            const int r = q / p.D, f = q - r * p.D;
+            x[r * W + f] = double(obs_feature<TASK, Real>(c, view, r, f, p.bdim));
+        }
+        __syncwarp();
+        // FeedforwardWeights::forward (policy.hpp:95-116) for all robots at once: a lane owns
+        // (robot, neuron) outputs and runs up to four of them as independent accumulation chains
+        for (int l = 0; l < p.net.num_layers; ++l) {
+            const int nin = p.net.in[l], nout = p.net.out[l], act = p.net.act[l];
+            const double* Wt = p.wT + p.net.w_off[l];
+            const double* bb = p.bias + p.net.b_off[l];
+            const int total = N * nout;
+            for (int b0 = lane; b0 < total; b0 += 128) {
+                int ro[4], oo[4];
+                double acc[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int idx = b0 + 32 * u;
+                    const int idc = idx < total ? idx : b0;
+                    ro[u] = idc / nout;
+                    oo[u] = idc - ro[u] * nout;
+                    acc[u] = __ldg(bb + oo[u]);
                 }
-                __syncwarp();
-                cur ^= 1;
-            }
-            if (lane == 0) {  // Policy::act (policy.hpp:456-480)
-                const double* lg = sm.h[cur];
-                int a = 0;
-                if (p.net.greedy) {
-                    for (int k = 1; k < 5; ++k)
-                        if (lg[k] > lg[a]) a = k;
-                } else {
-                    double mx = lg[0];
-                    for (int k = 0; k < 5; ++k) mx = mx < lg[k] ? lg[k] : mx;  // std::max
-                    double pr[5], z = 0.0;
-                    for (int k = 0; k < 5; ++k) {
-                        pr[k] = exp(__dsub_rn(lg[k], mx));
-                        z = __dadd_rn(z, pr[k]);
-                    }
-                    Rng rng{fork_key(fork_key(pkey, static_cast<uint64_t>(step)), static_cast<uint64_t>(r)), 0};
-                    double u = __dmul_rn(rng.uniform(), z);
-                    a = 4;
-                    for (int k = 0; k < 5; ++k) {
-                        u = __dsub_rn(u, pr[k]);
-                        if (u <= 0.0) {
-                            a = k;
-                            break;
-                        }
-                    }
+                for (int i = 0; i < nin; ++i) {
+                    const double* wrow = Wt + static_cast<long long>(i) * nout;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        acc[u] = __dadd_rn(acc[u], __dmul_rn(__ldg(wrow + oo[u]), x[ro[u] * W + i]));
                 }
-                p.actions[e * N + r] = static_cast<int8_t>(a);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    double v = acc[u];
+                    if (act == MRSIM_ACT_RELU) v = v > 0 ? v : 0.0;
+                    else if (act == MRSIM_ACT_TANH) v = tanh(v);
+                    if (b0 + 32 * u < total) y[ro[u] * W + oo[u]] = v;
+                }
             }
             __syncwarp();
+            double* t = x;
+            x = y;
+            y = t;
+        }
+        if (lane < N) {  // Policy::act (policy.hpp:456-480), lane r for robot r
+            const double* lg = x + lane * W;
+            int a = 0;
+            if (p.net.greedy) {
+                for (int k = 1; k < 5; ++k)
+                    if (lg[k] > lg[a]) a = k;
+            } else {
+                double mx = lg[0];
+                for (int k = 0; k < 5; ++k) mx = mx < lg[k] ? lg[k] : mx;  // std::max
+                double pr[5], z = 0.0;
+                for (int k = 0; k < 5; ++k) {
+                    pr[k] = exp(__dsub_rn(lg[k], mx));
+                    z = __dadd_rn(z, pr[k]);
+                }
+                Rng rng{fork_key(fork_key(pkey, static_cast<uint64_t>(step)), static_cast<uint64_t>(lane)), 0};
+                double u = __dmul_rn(rng.uniform(), z);
+                a = 4;
+                for (int k = 0; k < 5; ++k) {
+                    u = __dsub_rn(u, pr[k]);
+                    if (u <= 0.0) {
+                        a = k;
+                        break;
+                    }
+                }
+            }
+            p.actions[e * N + lane] = static_cast<int8_t>(a);
         }
     }
 }

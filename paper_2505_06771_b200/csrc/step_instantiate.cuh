@@ -113,9 +113,17 @@ cudaError_t launch_reset<double, MRSIM_TASK_ID>(const mrsim_dev::ResetParams<dou
 
 template <class Real>
 static cudaError_t launch_policy_any(const mrsim_dev::PolicyParams<Real>& p, cudaStream_t s) {
-    const long long want = (p.B + mrsim_dev::kPolicyWarps - 1) / mrsim_dev::kPolicyWarps;
+    int warps = mrsim_dev::kPolicyWarps;  // fewer warps per block when one env's buffers are large
+    while (warps > 1 && warps * p.warp_bytes > 200 * 1024) warps >>= 1;
+    const long long want = (p.B + warps - 1) / warps;
     const unsigned grid = static_cast<unsigned>(want < 148 * 64 ? want : 148 * 64);
-    mrsim_dev::policy_kernel<Real, MRSIM_TASK_ID><<<grid, 32 * mrsim_dev::kPolicyWarps, 0, s>>>(p);
+    const int smem = warps * p.warp_bytes;
+    auto k = mrsim_dev::policy_kernel<Real, MRSIM_TASK_ID>;
+    if (smem > 48 * 1024) {
+        const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+    }
+    k<<<grid, 32 * warps, smem, s>>>(p);
     return cudaGetLastError();
 }
 template <>
