@@ -12,7 +12,10 @@
 //
 // For throughput the Engine also exposes the device-resident path
 // (reset_episodes / step with device buffers) that skips the per-call state
-// round trip the pure signature implies.
+// round trip the pure signature implies. mrsim::cuda::run_episodes(run) is the
+// harness's run_episodes (harness.hpp:216-300) on the device, with the policy
+// on device (mrsim::cuda::set_policy) and the rows recorded by the step; it
+// returns the reference's RunSummary and writes the reference's trajectory file.
 #pragma once
 
 #include <cstring>
@@ -22,7 +25,11 @@
 #include <variant>
 #include <vector>
 
+#include <algorithm>
+
 #include "mrsim/batch.hpp"
+#include "mrsim/harness.hpp"
+#include "mrsim/policy.hpp"
 #include "mrsim_cuda.h"
 
 namespace mrsim::cuda {
@@ -403,6 +410,96 @@ inline std::pair<BatchWorldState, std::vector<StepOutput>> step_batch(Engine& en
         o.metrics = next.envs.back().metrics;
     }
     return {std::move(next), std::move(outs)};
+}
+
+/// The device policy used by steps without host actions (Policy / PolicySpec,
+/// policy.hpp:17-57, 432-486): random (default), scripted_goal, prey_chaser, or
+/// a feedforward network read by the reference's own FeedforwardWeights::load.
+inline void set_policy(Engine& eng, const PolicySpec& spec) {
+    switch (spec.kind) {
+        case PolicyKind::Random: eng.check(mrsim_set_policy_random(eng.ctx())); return;
+        case PolicyKind::ScriptedGoal: eng.check(mrsim_set_policy_scripted(eng.ctx(), MRSIM_POLICY_SCRIPTED_GOAL)); return;
+        case PolicyKind::PreyChaser: eng.check(mrsim_set_policy_scripted(eng.ctx(), MRSIM_POLICY_PREY_CHASER)); return;
+        case PolicyKind::FeedforwardFile: {
+            const FeedforwardWeights w = FeedforwardWeights::load(spec.path);
+            std::vector<int32_t> dims, acts;
+            std::vector<double> flat;
+            for (const DenseLayer& l : w.layers) {
+                dims.push_back(l.in);
+                dims.push_back(l.out);
+                acts.push_back(l.activation == Activation::Relu ? MRSIM_ACT_RELU
+                               : l.activation == Activation::Tanh ? MRSIM_ACT_TANH : MRSIM_ACT_IDENTITY);
+                flat.insert(flat.end(), l.w.begin(), l.w.end());
+                flat.insert(flat.end(), l.b.begin(), l.b.end());
+            }
+            eng.check(mrsim_set_policy_feedforward(eng.ctx(), static_cast<int>(w.layers.size()), dims.data(),
+                                                   acts.data(), flat.data(), spec.greedy ? 1 : 0));
+            return;
+        }
+    }
+}
+
+/// run_episodes (harness.hpp:216-300) on the device: waves of run.batch
+/// episodes seeded derive_episode_seed(run.seed, episode), the policy producing
+/// each step's actions on device, every (episode, step, robot) row recorded by
+/// the step itself (mrsim_capture_*). Returns the reference's RunSummary (rows,
+/// per-episode stats) and writes the reference's trajectory file with its own
+/// build_header / write_trajectory.
+inline RunSummary run_episodes(const RunConfig& run, bool write_file = true, int device = 0) {
+    const ScenarioConfig cfg = resolve_scenario_config(run);
+    const PolicySpec spec = PolicySpec::parse(run.policy);
+    RunSummary summary;
+    summary.scenario = run.scenario;
+    summary.metric_name = scenario_metric_name(run.scenario);
+    const int N = cfg.num_robots, T = cfg.max_steps;
+    for (int wave_start = 0; wave_start < run.episodes; wave_start += run.batch) {
+        const int wave = std::min(run.batch, run.episodes - wave_start);
+        Engine eng(cfg, wave, device);
+        set_policy(eng, spec);
+        eng.check(mrsim_reset_episodes(eng.ctx(), run.seed, wave_start, wave, nullptr, nullptr));
+        eng.check(mrsim_capture_begin(eng.ctx(), T));
+        for (int t = 0; t < T; ++t) eng.check(mrsim_step(eng.ctx(), nullptr, nullptr, nullptr, nullptr, nullptr, nullptr));
+        eng.check(mrsim_sync(eng.ctx(), nullptr));
+        std::vector<mrsim_traj_record> rec(static_cast<std::size_t>(T) * wave * N);
+        eng.check(mrsim_capture_read(eng.ctx(), 0, wave, rec.data()));
+        const auto states = eng.download();
+        for (int e = 0; e < wave; ++e) {
+            double total = 0.0;
+            for (int t = 0; t < T; ++t) {
+                const mrsim_traj_record* at = rec.data() + (static_cast<std::size_t>(t) * wave + e) * N;
+                total += at[0].reward;
+                for (int r = 0; r < N; ++r) {
+                    TrajectoryRow row;
+                    row.env = wave_start + e;
+                    row.step = t;
+                    row.robot = r;
+                    row.x = at[r].x;
+                    row.y = at[r].y;
+                    row.theta = at[r].theta;
+                    row.action = at[r].action;
+                    row.reward = at[r].reward;
+                    row.done = at[r].done != 0;
+                    row.collisions = at[r].collisions;
+                    row.metric = at[r].metric;
+                    summary.rows.push_back(row);
+                }
+            }
+            const mrsim_env_state& s = states[static_cast<std::size_t>(e)];
+            EpisodeStats st;
+            st.total_reward = total;
+            st.final_metric = s.scenario_metric;
+            st.collisions = s.collisions;
+            st.success = s.success != 0;
+            st.min_pairwise_distance = s.min_pairwise_distance;
+            st.qp_infeasible = s.qp_infeasible;
+            summary.episodes.push_back(st);
+        }
+    }
+    if (write_file) {
+        summary.trajectory_path = run.out.empty() ? default_trajectory_path(run) : run.out;
+        write_trajectory(summary.trajectory_path, build_header(run, cfg), summary.rows);
+    }
+    return summary;
 }
 
 }  // namespace mrsim::cuda
