@@ -314,3 +314,37 @@ def test_host_api_matches_device_step(pinned):
     with pytest.raises(m.InvalidArgument, match=r"invalid action 300 for environment 40000, robot 2"):
         ga.step_host(act_buf, out=outs)
     assert ga.get_states(40000, 1)[0].x[0] == before
+
+
+# Every kernel variant and the extremes of the team size: N = 1 (no pair rows), 2, 7 (L=8, 4 pair
+# slots per lane), 13 and 16 (L=16, 8 pair slots; 16 = MRSIM_MAX_ROBOTS), and rware with 8 slots
+# (the 16-obstacle-slot variant).
+@pytest.mark.parametrize("n", [1, 2, 7, 13, 16])
+def test_team_size_extremes_match_reference(n, ref):
+    cfg, st = _teacher_forced(ref, "navigation", n, True, 0, 40, B=24)
+    assert st["discrete"] == [], st["discrete"][:5]
+    assert st["pose"] <= 1e-9 and st["angle"] <= 1e-8, st
+    assert st["reward_bad"] == 0
+
+
+def test_rware_wide_layout_variant_matches_reference(ref):
+    slots = [-1.2, -0.4, -0.8, -0.4, -0.4, -0.4, 0.0, -0.4, -1.2, 0.4, -0.8, 0.4, -0.4, 0.4, 0.0, 0.4]
+    cfg = m.make_default_config("rware")
+    cfg.set_num_robots(4)
+    cfg.set_layout("rware.slots", slots)
+    sp = ref.spec("rware", num_robots=4, layout={"rware.slots": slots})
+    B = 32
+    seeds = [m.derive_episode_seed(9, e) for e in range(B)]
+    rb = ref.RefBatch(sp)
+    rb.reset(seeds)
+    gb = m.CudaEnvBatch(cfg, B, fp64=True)
+    for t in range(cfg.raw.max_steps):
+        st0 = rb.get_states()
+        acts = rb.random_actions()
+        gb.set_states(list(st0))
+        gobs, grew, gdone = gb.step_host(acts)
+        robs, rrew, rdone, _ = rb.step(acts)
+        pe, ae, bad, re_ = compare_states(gb.get_states(), rb.get_states(), 4, 0, 0, 0)
+        assert not bad and pe <= 1e-9 and ae <= 1e-8, (t, pe, ae, bad[:3])
+        assert np.array_equal(gdone, rdone)
+        assert np.all(np.abs(grew - rrew) <= 1e-9 * np.maximum(1.0, np.abs(rrew)))
