@@ -348,3 +348,50 @@ def test_rware_wide_layout_variant_matches_reference(ref):
         assert not bad and pe <= 1e-9 and ae <= 1e-8, (t, pe, ae, bad[:3])
         assert np.array_equal(gdone, rdone)
         assert np.all(np.abs(grew - rrew) <= 1e-9 * np.maximum(1.0, np.abs(rrew)))
+
+
+@pytest.mark.parametrize("task,n", [("navigation", 4), ("arctic_transport", 10)])
+def test_action_noise_matches_reference(task, n, ref):
+    """framework.hpp:96-108: waypoint noise drawn from the step stream (2 draws per robot)."""
+    cfg, sp = make_cfgs(ref, task, n)
+    cfg.action_noise_scale = 0.3
+    sp.noise = 0.3
+    B = 32
+    seeds = [m.derive_episode_seed(13, e) for e in range(B)]
+    rb = ref.RefBatch(sp)
+    rb.reset(seeds)
+    gb = m.CudaEnvBatch(cfg, B, fp64=True)
+    gb.reset_seeds(seeds)
+    for t in range(40):
+        acts = rb.random_actions()
+        _, grew, gdone = gb.step_host(acts)
+        _, rrew, rdone, _ = rb.step(acts)
+        pe, ae, bad, re_ = compare_states(gb.get_states(), rb.get_states(), n, 0, 0, 0)
+        assert not bad and pe <= 1e-8 and ae <= 1e-7, (t, pe, ae, bad[:3])
+        assert np.all(np.abs(grew - rrew) <= 1e-9 * np.maximum(1.0, np.abs(rrew)))
+
+
+def test_auto_reset_continues_with_the_next_wave(ref):
+    """In-kernel auto-reset: a done env restarts as episode + B, i.e. exactly
+    the reference's next run_episodes wave (harness.hpp:227-232)."""
+    cfg, sp = make_cfgs(ref, "navigation", 4, max_steps=12)
+    B = 32
+    gb = m.CudaEnvBatch(cfg, B, fp64=True, auto_reset=True)
+    gb.reset_episodes(root_seed=5, first_episode=0, episode_stride=B)
+    for wave in range(2):
+        rb = ref.RefBatch(sp)
+        seeds = [m.derive_episode_seed(5, wave * B + e) for e in range(B)]
+        rb.reset(seeds)
+        for t in range(12):
+            acts = rb.random_actions()
+            _, grew, gdone = gb.step_host(acts)
+            _, rrew, rdone, _ = rb.step(acts)
+            assert np.array_equal(gdone, rdone)
+            assert np.all(np.abs(grew - rrew) <= 1e-9 * np.maximum(1.0, np.abs(rrew)))
+            if t < 11:  # the done step's state is already the next episode's reset
+                pe, ae, bad, _ = compare_states(gb.get_states(), rb.get_states(), 4, 0, 0, 0)
+                assert not bad and pe <= 1e-8, (wave, t, pe, bad[:3])
+    st = gb.get_states()
+    assert [s.episode for s in st] == [2 * B + e for e in range(B)]
+    assert all(s.step_index == 0 for s in st)
+    assert gb.stats()["episodes"] == 2 * B
