@@ -161,3 +161,26 @@ def test_prey_chaser_policy_matches_reference(ref):
     nav = m.CudaEnvBatch(m.make_default_config("navigation"), 2)
     with pytest.raises(m.InvalidArgument, match="prey_chaser policy only applies to predator_prey"):
         nav.set_policy("prey_chaser")
+
+
+@pytest.mark.parametrize("spec", ["scripted_goal", "mlp"])
+def test_policies_run_in_fp32_mode(spec, ref):
+    """The fp32 fast mode drives the same device policies (observations / geometry in the state
+    precision); actions stay in range and mostly agree with the fp64 path on identical states."""
+    import torch
+    cfg, _ = make_cfgs(ref, "navigation", 4)
+    B = 64
+    seeds = [m.derive_episode_seed(31, e) for e in range(B)]
+    g32, g64 = m.CudaEnvBatch(cfg, B, fp64=False), m.CudaEnvBatch(cfg, B, fp64=True)
+    g32.reset_seeds(seeds)
+    g64.reset_seeds(seeds)
+    pol = spec if spec != "mlp" else m.FeedforwardWeights.random([cfg.obs_dim, 32, 5], ["relu", "identity"], seed=2)
+    g32.set_policy(pol)
+    g64.set_policy(pol)
+    a32 = g32.policy_actions().cpu().numpy()
+    a64 = g64.policy_actions().cpu().numpy()
+    assert a32.min() >= 0 and a32.max() <= 4
+    assert np.mean(a32 == a64) >= 0.95
+    g32.step(None)
+    torch.cuda.synchronize()
+    g32.sync()

@@ -395,3 +395,13 @@ def test_auto_reset_continues_with_the_next_wave(ref):
     assert [s.episode for s in st] == [2 * B + e for e in range(B)]
     assert all(s.step_index == 0 for s in st)
     assert gb.stats()["episodes"] == 2 * B
+
+
+@pytest.mark.parametrize("task,n,controller", [("random_waypoints", 4, 1), ("navigation", 4, 1),
+                                               ("random_waypoints", 4, 0)])
+def test_fp32_fast_mode_new_paths_track_reference(task, n, controller, ref):
+    """fp32 opt-in mode on the pose controller / random_waypoints paths: one teacher-forced tick
+    agrees to fp32 accuracy (same bound as the benchmark tasks)."""
+    cfg, st = _teacher_forced(ref, task, n, False, 1, 40, max_steps=60, controller=controller)
+    assert st["pose"] <= 2e-6 and st["angle"] <= 4e-5, st
+    assert len(st["discrete"]) <= 1, st["discrete"][:5]
