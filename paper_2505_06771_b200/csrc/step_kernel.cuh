@@ -496,8 +496,11 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
     BarrierRows<Real, L, MP, MO> rows;
     init_rows(rows, sm.rc, lane, N, p.k.cap);
     const int total_rows_base = rows.P + 4 * N + 4 * N;
+    __shared__ double het_flat[MRSIM_MAX_ROBOTS * MRSIM_MAX_HET_COLS];  // het_augment, full team, feature order
+    for (int k = threadIdx.x; k < c.het_rows * c.het_cols; k += blockDim.x) het_flat[k] = c.het[k / c.het_cols][k % c.het_cols];
+    __syncthreads();
     const EnvView<Real> view{sm.xs, sm.ys, sm.ts, sm.tf, sm.ti, N, sm.drones, p.prey_off,
-                             TASK == MRSIM_TASK_ARCTIC_TRANSPORT ? sm.dcell : nullptr};
+                             TASK == MRSIM_TASK_ARCTIC_TRANSPORT ? sm.dcell : nullptr, het_flat};
     const long long stride = static_cast<long long>(gridDim.x) * gpb;
 
     for (long long e0 = p.e_begin + static_cast<long long>(blockIdx.x) * gpb + (gib & ~(G - 1)); e0 < p.e_end;
@@ -745,9 +748,9 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
             float* wst = reinterpret_cast<float*>(smem_raw + gpb * p.smem_bytes_per_group) +
                          (threadIdx.x >> 5) * p.obs_stage;
             float* mine = wst + (gib & (G - 1)) * ND;
-            for (int q = lane; q < ND; q += L) {
-                const int r = q / p.D;
-                mine[q] = static_cast<float>(obs_feature<TASK, Real>(c, view, r, q - r * p.D, p.bdim));
+            for (int q = lane, r = lane / p.D, f = lane - (lane / p.D) * p.D; q < ND; q += L) {
+                mine[q] = static_cast<float>(obs_feature<TASK, Real>(c, view, r, f, p.bdim));
+                for (f += L; f >= p.D; f -= p.D) ++r;
             }
             __syncwarp();
             const long long left = p.e_end - e0;
@@ -757,9 +760,9 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
             __syncwarp();
         } else if (p.obs && !skip) {
             float* o = p.obs + e * ND;
-            for (int q = lane; q < ND; q += L) {
-                const int r = q / p.D;
-                o[q] = static_cast<float>(obs_feature<TASK, Real>(c, view, r, q - r * p.D, p.bdim));
+            for (int q = lane, r = lane / p.D, f = lane - (lane / p.D) * p.D; q < ND; q += L) {
+                o[q] = static_cast<float>(obs_feature<TASK, Real>(c, view, r, f, p.bdim));
+                for (f += L; f >= p.D; f -= p.D) ++r;
             }
         }
 

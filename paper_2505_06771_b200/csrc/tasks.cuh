@@ -253,6 +253,7 @@ struct EnvView {
     const int* drones;  // arctic: robot index of the k-th drone (robot-index order), else unused
     const double* prey_off;  // predator_prey: 8 candidate offsets (x, y), else unused
     const int* dcell = nullptr;  // arctic: (col, row) of the k-th drone, cached per env (or null)
+    const double* het_flat = nullptr;  // full-team het_augment values in feature order (or null)
 };
 
 // arctic: the grid cell under a robot, with the observation's truncating casts
@@ -608,6 +609,7 @@ __device__ Real obs_feature(const mrsim_cfg& c, const EnvView<Real>& v, int r, i
     if (q >= bdim) {  // het_augment
         const int k = q - bdim;
         if (c.het_obs_mode == MRSIM_HET_OBS_OWN) return Real(c.het[r][k]);
+        if (v.het_flat) return Real(v.het_flat[k]);
         return Real(c.het[k / c.het_cols][k % c.het_cols]);
     }
     if (TASK == MRSIM_TASK_RANDOM_WAYPOINTS) {  // random_waypoints.hpp:70-76: own pose + target
