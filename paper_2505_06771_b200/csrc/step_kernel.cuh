@@ -137,6 +137,7 @@ struct BarrierRows {
     static constexpr int kU = 3 * MP + 4 + 3 * MO;
     static constexpr int kFields = kU + 2;
     Real* rc;
+    unsigned char* ptab;  // pair p -> robots (ptab[2p], ptab[2p+1]), shared by the block
     int N, P, off_obs, off_box;
     int npair;
     int pi[MP], pj[MP];
@@ -228,7 +229,8 @@ struct BarrierRows {
             dsc.cx = F(3 * s, owner);
             dsc.cy = F(3 * s + 1, owner);
             dsc.h = F(3 * s + 2, owner);
-            pair_of(p, N, dsc.r0, dsc.r1);
+            dsc.r0 = ptab[2 * p];
+            dsc.r1 = ptab[2 * p + 1];
         } else if (p < off_obs) {  // wall w of robot r
             const int q = p - P, w = q & 3;
             dsc.r0 = q >> 2;
@@ -298,8 +300,10 @@ struct BarrierRows {
 };
 
 template <class Real, int L, int MP, int MO>
-__device__ __forceinline__ void init_rows(BarrierRows<Real, L, MP, MO>& rows, Real* rc, int lane, int N, Real cap) {
+__device__ __forceinline__ void init_rows(BarrierRows<Real, L, MP, MO>& rows, Real* rc, unsigned char* ptab, int lane,
+                                          int N, Real cap) {
     rows.rc = rc;
+    rows.ptab = ptab;
     rows.N = N;
     rows.P = N * (N - 1) / 2;
     rows.off_obs = rows.P + 4 * N;
@@ -315,6 +319,8 @@ __device__ __forceinline__ void init_rows(BarrierRows<Real, L, MP, MO>& rows, Re
         if (pidx < rows.P) {
             pair_of(pidx, N, i, j);
             rows.npair = s + 1;
+            ptab[2 * pidx] = static_cast<unsigned char>(i);  // every group of the block writes the same table
+            ptab[2 * pidx + 1] = static_cast<unsigned char>(j);
         }
         rows.pi[s] = i;
         rows.pj[s] = j;
@@ -494,7 +500,8 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
     const int ri = vl ? lane : 0;
 
     BarrierRows<Real, L, MP, MO> rows;
-    init_rows(rows, sm.rc, lane, N, p.k.cap);
+    __shared__ unsigned char pair_tab[MRSIM_MAX_ROBOTS * (MRSIM_MAX_ROBOTS - 1)];
+    init_rows(rows, sm.rc, pair_tab, lane, N, p.k.cap);
     const int total_rows_base = rows.P + 4 * N + 4 * N;
     __shared__ double het_flat[MRSIM_MAX_ROBOTS * MRSIM_MAX_HET_COLS];  // het_augment, full team, feature order
     for (int k = threadIdx.x; k < c.het_rows * c.het_cols; k += blockDim.x) het_flat[k] = c.het[k / c.het_cols][k % c.het_cols];

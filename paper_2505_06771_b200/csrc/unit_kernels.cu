@@ -116,7 +116,8 @@ __global__ void __launch_bounds__(128) barrier_batch_kernel(const __grid_constan
     int status = kQpOptimal;
     if (c.barrier_enabled) {
         BarrierRows<Real, L, MP, MO> rows;
-        init_rows(rows, rcache, lane, N, k.cap);
+        __shared__ unsigned char pair_tab[MRSIM_MAX_ROBOTS * (MRSIM_MAX_ROBOTS - 1)];
+        init_rows(rows, rcache, pair_tab, lane, N, k.cap);
         // static obstacles with masks (barrier.hpp:106-119), radius inflated (barrier.hpp:157)
         int obs_rows = 0;
         const double infl = c.projection_distance + c.discrete_margin;
@@ -204,7 +205,7 @@ cudaError_t run_barrier(const mrsim_cfg& c, int count, const double* dp, const d
                    ~15;
     const int grid = (count + gpb - 1) / gpb;
     auto kern = mrsim_dev::barrier_batch_kernel<Real, L>;
-    if (sg * gpb > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sg * gpb);
+    if (sg * gpb > 46 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sg * gpb);
     kern<<<grid, block, sg * gpb>>>(c, k, count, N, dp, dn, nobs, dobs, dm, dc, di, dco, sg);
     return cudaGetLastError();
 }
