@@ -33,6 +33,7 @@ struct mrsim_ctx {
     EnvStats st{};
     unsigned long long* d_err = nullptr;
     long long* d_err_serial = nullptr;
+    unsigned* d_ticket = nullptr;
     int cur = 0;
     long long serial = 0;
     int hist_in[64] = {0};
@@ -337,6 +338,7 @@ StepParams<Real> step_params(mrsim_ctx* ctx, DevState<Real>* s, const int8_t* ac
     p.next_obs = next_obs;
     p.err = ctx->d_err;
     p.err_serial = ctx->d_err_serial;
+    p.ticket = ctx->d_ticket;
     p.serial = ctx->serial;
     p.B = ctx->B;
     p.e_begin = 0;
@@ -777,8 +779,11 @@ int mrsim_create(const mrsim_cfg* cfg, int device, int64_t num_envs, uint32_t fl
         std::vector<double> inf(ctx->B, INFINITY);
         cudaMemcpy(ctx->st.min_dist, inf.data(), 8 * ctx->B, cudaMemcpyHostToDevice);
     }
-    if ((e = cudaMalloc(&ctx->d_err, 16)) != cudaSuccess) return bail(e, "cudaMalloc err");
+    // error word, its step serial, then the step kernel's two warp-task counters
+    if ((e = cudaMalloc(&ctx->d_err, 32)) != cudaSuccess) return bail(e, "cudaMalloc err");
     ctx->d_err_serial = reinterpret_cast<long long*>(ctx->d_err + 1);
+    ctx->d_ticket = reinterpret_cast<unsigned*>(ctx->d_err + 2);
+    cudaMemset(ctx->d_ticket, 0, 8);
     const unsigned long long none = ~0ull;
     cudaMemcpy(ctx->d_err, &none, sizeof none, cudaMemcpyHostToDevice);
     cudaMemset(ctx->d_err_serial, 0xff, 8);

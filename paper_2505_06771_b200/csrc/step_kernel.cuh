@@ -29,6 +29,9 @@
 #ifndef MRSIM_SMALL_MINB
 #define MRSIM_SMALL_MINB 4
 #endif
+#ifndef MRSIM_DYN_SCHED
+#define MRSIM_DYN_SCHED 1
+#endif
 #ifndef MRSIM_MIN_BLOCKS
 #define MRSIM_MIN_BLOCKS(L, TASK) ((L) >= 16 ? 3 : (TASK) == MRSIM_TASK_RWARE ? MRSIM_RW_MINB : MRSIM_SMALL_MINB)
 #endif
@@ -79,6 +82,7 @@ struct StepParams {
     float* next_obs;        // [B][N][D] or nullptr
     unsigned long long* err;
     long long* err_serial;
+    unsigned* ticket;       // [2] warp-task counters, used by alternate steps (serial & 1)
     long long serial;
     long long B;
     long long e_begin, e_end;  // env range of this launch (the host API pipelines chunks of a step)
@@ -479,6 +483,10 @@ __host__ __device__ constexpr bool qp_fast_first_row(int L) {
 template <class Real, int L, int MP, int MO, int TASK>
 __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(const __grid_constant__ StepParams<Real> p) {
     constexpr int G = 32 / L;  // envs per warp
+    // Dynamic warp tasks: a warp takes the next G consecutive envs from a counter. Step k
+    // uses counter k & 1 and clears the other one for step k + 1 (stream order makes that
+    // safe: step k - 1, its last user, has finished).
+    if (MRSIM_DYN_SCHED && blockIdx.x == 0 && threadIdx.x == 0) p.ticket[(p.serial + 1) & 1] = 0u;
     if (*p.err != ~0ull) return;  // sticky device error: later steps are no-ops
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -510,8 +518,15 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
                              TASK == MRSIM_TASK_ARCTIC_TRANSPORT ? sm.dcell : nullptr, het_flat};
     const long long stride = static_cast<long long>(gridDim.x) * gpb;
 
-    for (long long e0 = p.e_begin + static_cast<long long>(blockIdx.x) * gpb + (gib & ~(G - 1)); e0 < p.e_end;
-         e0 += stride) {
+    auto next_task = [&](long long e_static) -> long long {
+        if (!MRSIM_DYN_SCHED) return e_static;
+        unsigned t = 0;
+        if ((threadIdx.x & 31) == 0) t = atomicAdd(p.ticket + (p.serial & 1), 1u);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        return p.e_begin + static_cast<long long>(t) * G;
+    };
+    for (long long e0 = next_task(p.e_begin + static_cast<long long>(blockIdx.x) * gpb + (gib & ~(G - 1)));
+         e0 < p.e_end; e0 = next_task(e0 + stride)) {
         const long long e_real = e0 + (gib & (G - 1));
         const bool ghost = e_real >= p.e_end;
         const long long e = ghost ? p.e_end - 1 : e_real;
