@@ -34,6 +34,7 @@ struct mrsim_ctx {
     unsigned long long* d_err = nullptr;
     long long* d_err_serial = nullptr;
     unsigned* d_ticket = nullptr;
+    long long scripted_launches = 0;
     int cur = 0;
     long long serial = 0;
     int hist_in[64] = {0};
@@ -217,6 +218,8 @@ cudaError_t scripted_launch(mrsim_ctx* ctx, const DevState<Real>& st, int8_t* ou
     p.kind = ctx->scripted;
     mrsim_dev::prey_offsets(ctx->cfg, p.prey_off);
     p.actions = out;
+    p.ticket = ctx->d_ticket + 2;
+    p.serial = ctx->scripted_launches++;
     return dispatch_scripted<Real>(ctx->cfg.task, p, s);
 }
 
@@ -782,8 +785,8 @@ int mrsim_create(const mrsim_cfg* cfg, int device, int64_t num_envs, uint32_t fl
     // error word, its step serial, then the step kernel's two warp-task counters
     if ((e = cudaMalloc(&ctx->d_err, 32)) != cudaSuccess) return bail(e, "cudaMalloc err");
     ctx->d_err_serial = reinterpret_cast<long long*>(ctx->d_err + 1);
-    ctx->d_ticket = reinterpret_cast<unsigned*>(ctx->d_err + 2);
-    cudaMemset(ctx->d_ticket, 0, 8);
+    ctx->d_ticket = reinterpret_cast<unsigned*>(ctx->d_err + 2);  // step kernel [2], scripted kernel [2]
+    cudaMemset(ctx->d_ticket, 0, 16);
     const unsigned long long none = ~0ull;
     cudaMemcpy(ctx->d_err, &none, sizeof none, cudaMemcpyHostToDevice);
     cudaMemset(ctx->d_err_serial, 0xff, 8);

@@ -6,6 +6,12 @@
 // Reference paths below are relative to /root/reference/proj/include/mrsim.
 #pragma once
 
+// Dynamic work distribution in the persistent kernels (step, scripted planner): warps take
+// their next task from a per-launch counter instead of a static grid stride (A/B switch).
+#ifndef MRSIM_DYN_SCHED
+#define MRSIM_DYN_SCHED 1
+#endif
+
 #include <cstdint>
 #include <cuda_runtime.h>
 

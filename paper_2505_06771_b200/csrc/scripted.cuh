@@ -382,6 +382,8 @@ struct ScriptedParams {
     int kind;  // MRSIM_POLICY_SCRIPTED_GOAL / MRSIM_POLICY_PREY_CHASER
     double prey_off[16];
     int8_t* actions;
+    unsigned* ticket;  // [2] env counters, used by alternate launches (serial & 1)
+    long long serial;  // launch count of this context's scripted kernel
 };
 
 template <class Real, int TASK>
@@ -392,8 +394,18 @@ __global__ void __launch_bounds__(32 * kPolicyWarps) scripted_kernel(const __gri
     const mrsim_cfg& c = p.c;
     const int N = p.N;
     const double travel = c.si_max_speed * c.dt * c.sub_steps;  // policy.hpp:246
+    // Dynamic env tasks (planner cost varies widely per env): a warp takes the next env from
+    // counter serial & 1; this launch clears the other one for the next launch (stream order).
+    if (MRSIM_DYN_SCHED && blockIdx.x == 0 && threadIdx.x == 0) p.ticket[(p.serial + 1) & 1] = 0u;
+    auto next_env = [&](long long e_static) -> long long {
+        if (!MRSIM_DYN_SCHED) return e_static;
+        unsigned t = 0;
+        if (lane == 0) t = atomicAdd(p.ticket + (p.serial & 1), 1u);
+        return static_cast<long long>(__shfl_sync(0xffffffffu, t, 0));
+    };
     const long long stride = static_cast<long long>(gridDim.x) * kPolicyWarps;
-    for (long long e = static_cast<long long>(blockIdx.x) * kPolicyWarps + wib; e < p.B; e += stride) {
+    for (long long e = next_env(static_cast<long long>(blockIdx.x) * kPolicyWarps + wib); e < p.B;
+         e = next_env(e + stride)) {
         __syncwarp();
         if (lane < N) {
             sm.xs[lane] = double(p.s.px[e * N + lane]);

@@ -29,9 +29,6 @@
 #ifndef MRSIM_SMALL_MINB
 #define MRSIM_SMALL_MINB 4
 #endif
-#ifndef MRSIM_DYN_SCHED
-#define MRSIM_DYN_SCHED 1
-#endif
 #ifndef MRSIM_MIN_BLOCKS
 #define MRSIM_MIN_BLOCKS(L, TASK) ((L) >= 16 ? 3 : (TASK) == MRSIM_TASK_RWARE ? MRSIM_RW_MINB : MRSIM_SMALL_MINB)
 #endif
