@@ -277,8 +277,9 @@ int mrsim_reset_episodes(mrsim_ctx* ctx, uint64_t root_seed, int64_t first_episo
  * Asynchronous on `stream`. A device-side error (invalid action, coincident
  * robots, spawn failure) is sticky: it is returned by the next synchronous
  * call (mrsim_sync) and later steps become no-ops. Each call flips the
- * context's state buffers and its warp-task counter (step serial & 1), so a
- * CUDA graph capturing mrsim_step must capture an even number of calls. */
+ * context's state buffers and its warp-task counter (step serial & 1; a
+ * scripted policy's planner kernel flips its own counter once per call too), so
+ * a CUDA graph capturing mrsim_step must capture an even number of calls. */
 int mrsim_step(mrsim_ctx* ctx, const int8_t* actions_dev, float* obs_dev, float* reward_dev,
                uint8_t* done_dev, float* next_obs_dev, void* stream);
 /* The same step with HOST buffers (the reference's std::vector<int> actions
