@@ -16,6 +16,8 @@
 // flip only at a near-tie.
 #pragma once
 
+#include <cstddef>
+
 #include "policy.cuh"
 
 namespace mrsim_dev {
@@ -29,8 +31,15 @@ struct ScriptedSmem {
     int drones[MRSIM_MAX_ROBOTS];
     unsigned blocked[kGridWords], frontier[kGridWords], visited[kGridWords], next[kGridWords];
     unsigned colE[kGridWords], colW[kGridWords];  // cells that have an east / west neighbour column
-    unsigned short dist[kGridMaxCells];  // BFS level + 1 (0 = unreached)
+    unsigned short dist[kGridMaxCells];  // BFS level + 1 (0 = unreached); last: see scripted_smem_stride
 };
+
+// Per-warp shared-memory footprint for an arena of `cells` planner cells: `dist` (the last member)
+// is cut to the grid's whole 32-cell words, so a 3.2 x 2 m arena (2,560 cells) takes 9.2 KB instead
+// of 12.2 KB per warp and six 4-warp blocks fit an SM (registers allow six; the full struct, four).
+__host__ __device__ constexpr int scripted_smem_stride(int cells) {
+    return (static_cast<int>(offsetof(ScriptedSmem, dist)) + ((cells + 31) / 32) * 32 * 2 + 15) / 16 * 16;
+}
 
 struct Vec2d {
     double x, y;
@@ -384,13 +393,14 @@ struct ScriptedParams {
     int8_t* actions;
     unsigned* ticket;  // [2] env counters, used by alternate launches (serial & 1)
     long long serial;  // launch count of this context's scripted kernel
+    int smem_stride;   // bytes of shared memory per warp (scripted_smem_stride)
 };
 
 template <class Real, int TASK>
 __global__ void __launch_bounds__(32 * kPolicyWarps) scripted_kernel(const __grid_constant__ ScriptedParams<Real> p) {
     extern __shared__ __align__(16) unsigned char scr_smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    ScriptedSmem& sm = reinterpret_cast<ScriptedSmem*>(scr_smem)[wib];
+    ScriptedSmem& sm = *reinterpret_cast<ScriptedSmem*>(scr_smem + wib * p.smem_stride);
     const mrsim_cfg& c = p.c;
     const int N = p.N;
     const double travel = c.si_max_speed * c.dt * c.sub_steps;  // policy.hpp:246

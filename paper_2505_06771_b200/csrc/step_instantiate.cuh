@@ -139,13 +139,18 @@ template <class Real>
 static cudaError_t launch_scripted_any(const mrsim_dev::ScriptedParams<Real>& p, cudaStream_t s) {
     const long long want = (p.B + mrsim_dev::kPolicyWarps - 1) / mrsim_dev::kPolicyWarps;
     const unsigned grid = static_cast<unsigned>(want < 148 * 16 ? want : 148 * 16);
-    const int smem = static_cast<int>(sizeof(mrsim_dev::ScriptedSmem)) * mrsim_dev::kPolicyWarps;
+    // grid cells as mrsim_set_policy_scripted sizes them (0.05 m, policy.hpp:253-255)
+    const int cols = static_cast<int>((2.0 * p.c.arena_half_width) / 0.05);
+    const int rows = static_cast<int>((2.0 * p.c.arena_half_height) / 0.05);
+    mrsim_dev::ScriptedParams<Real> q = p;
+    q.smem_stride = mrsim_dev::scripted_smem_stride(cols * rows);
+    const int smem = q.smem_stride * mrsim_dev::kPolicyWarps;
     auto k = mrsim_dev::scripted_kernel<Real, MRSIM_TASK_ID>;
     if (smem > 48 * 1024) {
         const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
     }
-    k<<<grid, 32 * mrsim_dev::kPolicyWarps, smem, s>>>(p);
+    k<<<grid, 32 * mrsim_dev::kPolicyWarps, smem, s>>>(q);
     return cudaGetLastError();
 }
 template <>
