@@ -109,11 +109,24 @@ __global__ void __launch_bounds__(32 * kPolicyWarps) policy_kernel(const __grid_
                     oo[u] = idc - ro[u] * nout;
                     acc[u] = __ldg(bb + oo[u]);
                 }
-                for (int i = 0; i < nin; ++i) {
-                    const double* wrow = Wt + static_cast<long long>(i) * nout;
+                // chains live in this pass (warp-uniform): a small last layer (nav: 4 robots x 5
+                // actions = 20 outputs) needs one, not four
+                const int live = total - (b0 - lane);
+                if (live > 96) {
+                    for (int i = 0; i < nin; ++i) {
+                        const double* wrow = Wt + static_cast<long long>(i) * nout;
 #pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        acc[u] = __dadd_rn(acc[u], __dmul_rn(__ldg(wrow + oo[u]), x[ro[u] * W + i]));
+                        for (int u = 0; u < 4; ++u)
+                            acc[u] = __dadd_rn(acc[u], __dmul_rn(__ldg(wrow + oo[u]), x[ro[u] * W + i]));
+                    }
+                } else {
+                    for (int i = 0; i < nin; ++i) {
+                        const double* wrow = Wt + static_cast<long long>(i) * nout;
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (32 * u < live)
+                                acc[u] = __dadd_rn(acc[u], __dmul_rn(__ldg(wrow + oo[u]), x[ro[u] * W + i]));
+                    }
                 }
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
