@@ -112,7 +112,14 @@ __global__ void __launch_bounds__(32 * kPolicyWarps) policy_kernel(const __grid_
                 // chains live in this pass (warp-uniform): a small last layer (nav: 4 robots x 5
                 // actions = 20 outputs) needs one, not four
                 const int live = total - (b0 - lane);
-                if (live > 96) {
+                if (live > 96 && nout == 32) {
+                    // chain u is robot 4k+u, neuron `lane`: one weight serves all four chains
+                    for (int i = 0; i < nin; ++i) {
+                        const double w = __ldg(Wt + static_cast<long long>(i) * 32 + lane);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) acc[u] = __dadd_rn(acc[u], __dmul_rn(w, x[ro[u] * W + i]));
+                    }
+                } else if (live > 96) {
                     for (int i = 0; i < nin; ++i) {
                         const double* wrow = Wt + static_cast<long long>(i) * nout;
 #pragma unroll
