@@ -1,0 +1,39 @@
+"""Parity at exactly the benchmarked configurations (tests/scale_parity.py):
+
+* navigation N=4, B = 65,536 (BASELINE configs[1], the bench workload): every
+  env, auto-reset over 150 steps (three waves, so warps run several tasks per
+  launch and the in-kernel reset path is exercised), against the reference
+  stepping all 65,536 envs with WorkerPool(all cores).
+* material_transport N=10 and arctic_transport N=10 at B = 131,072 (the
+  per-GPU share of BASELINE configs[4]): a 768-env sample in three contiguous
+  slices spanning hundreds of warp tasks, across an episode boundary.
+
+Tolerances as in scale_parity: discrete bit-exact, poses 1e-8 m / 1e-7 rad.
+"""
+import pytest
+
+from scale_parity import run_full_batch, run_sampled
+from test_gpu_step import make_cfgs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.timeout(1800)
+def test_navigation_65536_envs_every_env_matches_reference(ref):
+    cfg, sp = make_cfgs(ref, "navigation", 4, max_steps=70)
+    rep = run_full_batch(ref, cfg, sp, 65536, 150)
+    print(rep)
+    assert rep["ok"], rep
+    assert rep["waves"] == 2 and rep["checks"] >= 15
+
+
+@pytest.mark.timeout(1800)
+@pytest.mark.parametrize("task,steps", [("material_transport", 90), ("arctic_transport", 120)])
+def test_n10_131072_envs_sample_matches_reference(task, steps, ref):
+    cfg, sp = make_cfgs(ref, task, 10)
+    B = 131072
+    ranges = [(0, 256), (B // 2 - 128, B // 2 + 128), (B - 256, B)]
+    rep = run_sampled(ref, cfg, sp, B, steps, ranges)
+    print(rep)
+    assert rep["ok"], rep
+    assert rep["waves"] == 1
