@@ -8,27 +8,36 @@ in-kernel auto-reset with the harness's wave seeding. One "step" = one
 batched env-step of every env (10 physics ticks each).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--task navigation --robots 4 --envs 65536] [--fp32]
+                  [--task navigation --robots 4 --envs 65536] [--fp32] [--verify]
 
 The product path computes in fp64 (bit-exact discrete outcomes vs the
-reference); --fp32 selects the fast mode.
+reference); --fp32 selects the non-parity fast mode.
 
-Under torchrun each rank drives one GPU with its own contiguous env slice
-(weak scaling, no collective in the step); the only cross-GPU traffic is the
-final all-reduce of the timing max and the episode statistics.
+Multi-GPU (BASELINE metric "at 1/2/4/8 B200"): one process per
+GPU, each with its own contiguous env slice (multigpu.Shard: weak scaling, no
+collective in the step); the only cross-GPU traffic is the all-reduce of the
+timing max and of the episode statistics (multigpu.reduce_stats). Under
+torchrun the ranks come from the environment; `--gpus N` without torchrun
+launches the N ranks itself (torch.distributed.run on 127.0.0.1). With fewer
+visible GPUs than ranks the ranks share devices over gloo (a functional
+check of the multi-rank path, not a scaling number).
 
 Timing: W warm-up steps, then K steps; each step is bracketed by CUDA events
-on the launching stream and the 126 MB L2 is flushed (a 512 MiB write)
-between steps, outside the events; the per-step device times are summed.
+on the launching stream and the 126 MB L2 is flushed (a 512 MiB read, so no
+dirty lines are written back inside the next step) between steps, outside
+the events; the per-step device times are summed, max over ranks.
 `e2e` is the same metric through the host-buffer C-ABI call
-(mrsim_step_host: actions H2D from pinned memory, obs/reward/done D2H,
-synchronous), wall-clock timed.
+(mrsim_step_host: int32 actions from pinned host memory, obs / reward / done
+to pinned host memory, synchronous), wall-clock timed, max over ranks.
+`--verify` then checks every env of the bench batch against the reference
+over 150 steps (tests/scale_parity.py; test infrastructure as the checker).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import time
@@ -39,6 +48,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 ARCTIC_SPAWN = [-1.55, -1.05, -0.9, 0.9]
+METRIC = "env-steps/sec (CBF on)"
 
 
 def parse():
@@ -52,15 +62,22 @@ def parse():
     ap.add_argument("--envs", type=int, default=65536, help="envs per GPU")
     ap.add_argument("--max-steps", type=int, default=70)
     ap.add_argument("--fp32", action="store_true",
-                    help="opt-in fp32 fast mode (forks from the reference at hold-rule near-ties)")
+                    help="opt-in fp32 fast mode (not parity-grade: forks from the reference at hold-rule near-ties)")
+    ap.add_argument("--env-per-thread", action="store_true",
+                    help="teams of <= 4 robots: one thread per env instead of the lane-per-robot kernel (A/B)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
     ap.add_argument("--e2e-steps", type=int, default=20)
-    ap.add_argument("--dist-backend", default="nccl", help="nccl (GPUs) or gloo (multi-rank smoke test)")
+    ap.add_argument("--dist-backend", default="auto",
+                    help="nccl | gloo | auto (nccl when every rank has its own GPU, else gloo)")
     ap.add_argument("--controller", default="unicycle_position", choices=["unicycle_position", "unicycle_pose"],
                     help="ControllerKind (framework.hpp:126)")
     ap.add_argument("--policy", default="random", choices=["random", "mlp", "scripted_goal", "prey_chaser"],
                     help="on-device policy producing each step's actions (mlp: a random 64-32 relu network)")
+    ap.add_argument("--no-flush", action="store_true", help="no L2 flush between timed steps (traffic windows)")
+    ap.add_argument("--verify", action="store_true",
+                    help="after the bench, check every env of the bench batch against the reference (150 steps)")
+    ap.add_argument("--dump-states", default="", help="write each rank's final env states to PATH.rank<r>.npz")
     return ap.parse_args()
 
 
@@ -69,6 +86,16 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def launch_ranks(a) -> int:
+    """`--gpus N` without torchrun: start the N ranks (one process per GPU) on 127.0.0.1."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def workload_name(a) -> str:
@@ -90,6 +117,15 @@ def build_cfg(a):
     cfg.set_controller(a.controller)
     cfg.validate()
     return cfg
+
+
+def bench_config(a, cfg, world: int) -> dict:
+    """The `config` object of both arms (same keys, same values)."""
+    return {"workload": workload_name(a), "task": a.task, "robots": a.robots, "envs_per_gpu": a.envs,
+            "global_envs": a.envs * world, "max_steps": a.max_steps, "sub_steps": int(cfg.raw.sub_steps),
+            "barrier": True, "auto_reset": True, "controller": a.controller, "policy": a.policy,
+            "parallelism": f"env-shard x{world}",
+            "l2": "flushed (512 MiB read) between timed steps; per-step CUDA events summed"}
 
 
 def ref_spec(a):
@@ -141,6 +177,55 @@ def algorithmic_flops_per_env_step(cfg) -> int:
     return cfg.raw.sub_steps * (82 * N + 28 * P) + 10 * N
 
 
+def measured_traffic(a, fp64: bool):
+    """dram__bytes_read.sum + dram__bytes_write.sum per step-kernel launch, averaged over a window of
+    consecutive launches of this bench loop (scripts/measure_traffic.sh, ncu; profiles/traffic_r02.json)."""
+    path = os.path.join(ROOT, "profiles", "traffic_r02.json")
+    if not os.path.exists(path):
+        return None
+    try:
+        rec = json.load(open(path)).get(f"{a.task}{a.robots}_{a.envs}_{'fp64' if fp64 else 'fp32'}")
+    except Exception:
+        return None
+    return rec
+
+
+def roofline(a, cfg, per_gpu: float, kernel_ms: float, fp64: bool, pipe_peak_tflops: float) -> dict:
+    """The binding roof is chosen by arithmetic intensity against the ridge point."""
+    peaks = {}
+    pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pk):
+        peaks = json.load(open(pk))
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    hbm_src = "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks else "fallback 6650 GB/s"
+    bpe = algorithmic_bytes_per_env_step(cfg, fp64)
+    fpe = algorithmic_flops_per_env_step(cfg)
+    ai = fpe / bpe
+    ridge = pipe_peak_tflops * 1e12 / (hbm_peak * 1e9)
+    gbs = per_gpu * bpe / 1e9
+    tflops = per_gpu * fpe / 1e12
+    pipe = "fp64" if fp64 else "fp32"
+    tr = measured_traffic(a, fp64)
+    envs_per_launch = a.envs
+    hbm = {"achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
+           "algorithmic_bytes_per_env_step": bpe, "algorithmic_bytes_per_launch": bpe * envs_per_launch,
+           "peak_source": hbm_src}
+    comp = {"achieved": tflops, "peak": pipe_peak_tflops, "unit": "TFLOP/s", "frac": tflops / pipe_peak_tflops,
+            "algorithmic_flops_per_env_step": fpe, "algorithmic_flops_per_launch": fpe * envs_per_launch,
+            "peak_source": f"measured {pipe} FMA-chain probe (mrsim_probe_fma_peak) on this GPU"}
+    bound_pipe = ai >= ridge
+    out = dict(comp if bound_pipe else hbm)
+    out["bound"] = f"{pipe}-pipe" if bound_pipe else "hbm"
+    out["arithmetic_intensity"] = ai
+    out["ridge_flop_per_byte"] = ridge
+    out["traffic"] = tr["bytes_per_launch"] if tr else None
+    out["traffic_window"] = tr
+    out["hbm"] = hbm
+    out[pipe] = comp
+    out["kernel_ms"] = kernel_ms
+    return out
+
+
 class ClockSampler:
     def __init__(self, gpu: int):
         self.path = f"/tmp/mrsim_clocks_{os.getpid()}.csv"
@@ -179,39 +264,56 @@ class ClockSampler:
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def dump_states(path: str, rank: int, shard, batch) -> None:
+    from paper_2505_06771_b200 import _abi  # noqa: F401
+
+    st = np.ctypeslib.as_array(batch.get_states())
+    np.savez(f"{path}.rank{rank}.npz", first_episode=shard.first_episode,
+             **{f: st[f] for f in ("x", "y", "theta", "step_index", "collisions", "rng_key", "episode",
+                                   "scenario_metric", "success", "min_pairwise_distance")})
+
+
 def main():
     a = parse()
     rank, world, local = dist_env()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(launch_ranks(a))
     if a.impl == "reference":
         return main_reference(a, rank, world)
 
     import torch
 
     import paper_2505_06771_b200 as m
+    from paper_2505_06771_b200.multigpu import Shard, reduce_stats
 
-    local = local % max(torch.cuda.device_count(), 1)
+    ndev = max(torch.cuda.device_count(), 1)
+    local = local % ndev
     torch.cuda.set_device(local)
+    backend = a.dist_backend if a.dist_backend != "auto" else ("nccl" if world <= ndev else "gloo")
     dist = None
     rdev = "cuda"
     if world > 1:
         import torch.distributed as dist
 
-        if a.dist_backend == "nccl":
+        if backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator / NVLS lines on stderr
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
-            dist.init_process_group(a.dist_backend)
+            dist.init_process_group(backend)
             rdev = "cpu"
+    shard = Shard(rank, world, a.envs)
     cfg = build_cfg(a)
     B = a.envs
-    batch = m.CudaEnvBatch(cfg, B, device=local, fp64=(not a.fp32), auto_reset=True)
-    batch.reset_episodes(root_seed=0, first_episode=rank * B, episode_stride=world * B)
+    batch = m.CudaEnvBatch(cfg, B, device=local, fp64=(not a.fp32), auto_reset=True, env_per_thread=a.env_per_thread)
+    batch.reset_episodes(root_seed=0, first_episode=shard.first_episode, episode_stride=shard.episode_stride)
     if a.policy == "mlp":
         batch.set_policy(m.FeedforwardWeights.random([cfg.obs_dim, 64, 32, 5], ["relu", "relu", "identity"], seed=1))
     elif a.policy != "random":
         batch.set_policy(a.policy)
     launches_per_step = 1 if a.policy == "random" else 2  # the policy kernel, then the step
     stream = torch.cuda.current_stream()
-    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    flush = torch.ones(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    sink = torch.empty((), dtype=torch.float32, device="cuda")
 
     for _ in range(max(a.warmup, 3)):
         batch.step(None)
@@ -225,7 +327,8 @@ def main():
     torch.cuda.synchronize()
     w0 = time.perf_counter()
     for k in range(a.steps):
-        flush.zero_()  # L2 flush outside the timed events
+        if not a.no_flush:
+            torch.sum(flush, dim=0, out=sink)  # L2 flush (read-only) outside the timed events
         starts[k].record(stream)
         batch.step(None)
         ends[k].record(stream)
@@ -243,16 +346,12 @@ def main():
     value = world * B * a.steps / (dev_ms / 1e3)
     kernel_ms = dev_ms / a.steps
 
-    # episode statistics: the only cross-GPU reduction (sum + min)
-    st = batch.stats()
-    red = torch.tensor([st["episodes"], st["sum_return"], st["sum_collisions"], st["sum_success"],
-                        st["sum_qp_infeasible"]], dtype=torch.float64, device=rdev)
-    mn = torch.tensor([st["min_pairwise_distance"]], dtype=torch.float64, device=rdev)
-    if dist:
-        dist.all_reduce(red)
-        dist.all_reduce(mn, op=dist.ReduceOp.MIN)
+    # episode statistics: the only cross-GPU reduction (sum + min), multigpu.reduce_stats
+    stats = reduce_stats(batch.stats(), device=rdev)
+    if a.dump_states:
+        dump_states(a.dump_states, rank, shard, batch)
 
-    # e2e through the host-buffer C-ABI call (one GPU's share, then scaled by world for the job)
+    # e2e through the host-buffer C-ABI call (every rank, max over ranks)
     e2e = None
     if a.e2e_steps > 0:
         rng = np.random.default_rng(rank)
@@ -262,8 +361,8 @@ def main():
         outs = (torch.empty((B, a.robots, cfg.obs_dim), dtype=torch.float32).pin_memory().numpy(),
                 torch.empty((B,), dtype=torch.float64).pin_memory().numpy(),
                 torch.empty((B,), dtype=torch.uint8).pin_memory().numpy())
-        hb = m.CudaEnvBatch(cfg, B, device=local, fp64=(not a.fp32), auto_reset=True)
-        hb.reset_episodes(root_seed=0, first_episode=rank * B, episode_stride=world * B)
+        hb = m.CudaEnvBatch(cfg, B, device=local, fp64=(not a.fp32), auto_reset=True, env_per_thread=a.env_per_thread)
+        hb.reset_episodes(root_seed=0, first_episode=shard.first_episode, episode_stride=shard.episode_stride)
         hb.step_host(acts_np[0], out=outs)
         if dist:
             dist.barrier()
@@ -281,30 +380,26 @@ def main():
                       "and writes obs / reward / done in place over the host link (zero-copy), then syncs"}
         hb.close()
 
+    verify = None
+    if a.verify and rank == 0:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import scale_parity  # test infrastructure: the checker (oracle/_ref)
+
+        refbind, sp = ref_spec(a)
+        verify = scale_parity.run_full_batch(refbind, cfg, sp, B, 150, device=local)
+        verify = {k: v for k, v in verify.items() if k not in ("discrete_mismatch",)} | {
+            "discrete_mismatch": {k: str(v) for k, v in verify["discrete_mismatch"].items()},
+            "what": f"every env of a {B}-env auto-reset batch vs the reference, 150 steps, fp64"}
+
     if rank == 0:
-        peaks = {}
-        pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
-        if os.path.exists(pk):
-            peaks = json.load(open(pk))
-        hbm_peak = peaks.get("hbm_gbs", 6650.0)
-        bpe = algorithmic_bytes_per_env_step(cfg, (not a.fp32))
-        fpe = algorithmic_flops_per_env_step(cfg)
-        per_gpu = value / world
-        achieved_gbs = per_gpu * bpe / 1e9
         fp64 = not a.fp32
+        per_gpu = value / world
         pipe_peak = m.lib().mrsim_probe_fma_peak(local, int(fp64)) / 1e12  # measured FMA-chain peak
-        traffic = None
-        tf = os.path.join(ROOT, "profiles", "traffic.json")
-        if os.path.exists(tf):
-            try:
-                traffic = json.load(open(tf)).get(f"{a.task}{a.robots}_{'fp64' if (not a.fp32) else 'fp32'}")
-            except Exception:
-                traffic = None
         cpu = None
-        if not a.no_cpu_baseline:
+        if not a.no_cpu_baseline and world == 1:
             cpu = cpu_reference_rate(a, a.cpu_seconds, B)
         line = {
-            "metric": "env-steps/sec (CBF on)",
+            "metric": METRIC,
             "value": value,
             "unit": "env-steps/s",
             "robot_steps_per_s": value * a.robots,
@@ -315,30 +410,25 @@ def main():
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,
-            "dtype": "f64" if (not a.fp32) else "f32",
+            "dtype": "f64" if fp64 else "f32",
             "data": "synthetic: harness random policy on device, derive_episode_seed(0, e) resets",
-            "config": {"workload": workload_name(a), "task": a.task, "robots": a.robots, "envs_per_gpu": B,
-                       "global_envs": B * world, "max_steps": a.max_steps, "sub_steps": cfg.raw.sub_steps,
-                       "barrier": True, "auto_reset": True, "parallelism": f"env-shard x{world}",
-                       "l2": "flushed (512 MiB write) between timed steps; per-step CUDA events summed"},
-            "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved_gbs / hbm_peak, "traffic": traffic,
-                         "algorithmic_bytes_per_env_step": bpe, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
-                         "pipe": {"pipe": "fp64" if fp64 else "fp32",
-                                  "achieved_tflops": per_gpu * fpe / 1e12, "peak_tflops": pipe_peak,
-                                  "frac": per_gpu * fpe / 1e12 / pipe_peak,
-                                  "algorithmic_flops_per_env_step": fpe,
-                                  "peak_source": "measured FMA-chain probe (mrsim_probe_fma_peak) on this GPU"}},
+            "config": bench_config(a, cfg, world),
+            "kernel": "one thread per env (env_step_kernel)" if (a.env_per_thread and a.robots <= 4 and a.task != "rware")
+                      else f"lane groups of {4 if a.robots <= 4 else (8 if a.robots <= 8 else 16)} (step_kernel)",
+            "roofline": roofline(a, cfg, per_gpu, kernel_ms, fp64, pipe_peak),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": a.steps * launches_per_step,
             "clocks": clk,
             "wall_s_timed_region": wall,
-            "episodes": {"completed": float(red[0].item()),
-                         "mean_return": float(red[1].item() / max(red[0].item(), 1)),
-                         "collisions": float(red[2].item()), "success": float(red[3].item()),
-                         "qp_infeasible": float(red[4].item()), "min_pairwise_distance": float(mn.item())},
+            "dist_backend": backend if world > 1 else None,
+            "episodes": {"completed": stats["episodes"], "mean_return": stats["mean_return"],
+                         "collisions": stats["sum_collisions"], "success": stats["sum_success"],
+                         "qp_infeasible": stats["sum_qp_infeasible"],
+                         "min_pairwise_distance": stats["min_pairwise_distance"]},
         }
+        if verify is not None:
+            line["verify"] = verify
         print(json.dumps(line), flush=True)
     batch.close()
     if dist:
@@ -352,8 +442,9 @@ def main_reference(a, rank, world):
     if not refbind.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libmrsim_ref.so not built"}))
         return
-    import paper_2505_06771_b200 as m  # noqa: F401  (seed derivation only)
+    import paper_2505_06771_b200 as m  # seed derivation and the config mirror (host-only calls)
 
+    cfg = build_cfg(a)
     rb = refbind.RefBatch(sp, workers=0)
     cores = refbind.lib().ref_pool_size(rb.h)
     B = min(a.envs, 2048)
@@ -368,12 +459,11 @@ def main_reference(a, rank, world):
     value = B * a.steps / t
     sample = f"{B} of {a.envs} envs per step x {a.steps} steps (step_batch, WorkerPool({cores}))"
     print(json.dumps({
-        "impl": "reference", "metric": "env-steps/sec (CBF on)", "value": value, "unit": "env-steps/s",
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "env-steps/s",
         "robot_steps_per_s": value * a.robots, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": t / a.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic: harness random policy, derive_episode_seed(0, e) resets",
-        "config": {"workload": workload_name(a), "task": a.task, "robots": a.robots, "envs_per_gpu": a.envs,
-                   "max_steps": a.max_steps, "barrier": True},
+        "config": bench_config(a, cfg, world),
         "cpu_baseline": {"value": value, "unit": "env-steps/s", "cores": cores, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

@@ -5,8 +5,13 @@
 //   auto [next, outs]  = mrsim::cuda::step_batch(engine, state, actions, cfg);
 //
 // A caller of mrsim::reset_batch / mrsim::step_batch switches backends by
-// holding a mrsim::cuda::Engine and calling these instead; types, value
-// semantics (step_batch is pure) and exception types are the reference's.
+// calling mrsim::cuda::reset_batch / step_batch with the reference's own
+// argument list (cfg, seeds, scenario, pool) / (state, actions, cfg, scenario,
+// pool) -- one device context per (config, batch size) is created on first use
+// and cached -- or by holding a mrsim::cuda::Engine explicitly. Types, value
+// semantics (step_batch is pure) and exception types are the reference's; the
+// caller's WorkerPool, when given, parallelises the host-side conversion of the
+// reference's per-env objects (BatchWorldState, StepOutput) around the device step.
 // Requires the reference headers on the include path (mrsim/batch.hpp) and
 // linking libmrsim_cuda.so.
 //
@@ -19,6 +24,9 @@
 #pragma once
 
 #include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -152,14 +160,16 @@ inline mrsim_cfg flatten(const ScenarioConfig& c) {
 }
 
 /// EnvState (scenario.hpp:78-84) <-> mrsim_env_state.
-inline mrsim_env_state to_record(const EnvState& s) {
-    mrsim_env_state o;
-    std::memset(&o, 0, sizeof o);
+/// Only the fields mrsim_set_env_states reads for the config's task are written
+/// (no 2 KB clear per env).
+inline void to_record(const EnvState& s, mrsim_env_state& o) {
     const int n = static_cast<int>(s.poses.size());
     o.num_robots = n;
     o.step_index = s.step_index;
     o.rng_key = s.base_rng.key;
+    o.seed = 0;
     o.episode = -1;
+    o.episode_return = 0.0;
     for (int i = 0; i < n; ++i) {
         o.x[i] = s.poses[i].x;
         o.y[i] = s.poses[i].y;
@@ -226,6 +236,11 @@ inline mrsim_env_state to_record(const EnvState& s) {
             }
         },
         s.scenario);
+}
+inline mrsim_env_state to_record(const EnvState& s) {
+    mrsim_env_state o;
+    std::memset(&o, 0, sizeof o);
+    to_record(s, o);
     return o;
 }
 
@@ -343,17 +358,37 @@ public:
         check(mrsim_get_env_states(ctx_, 0, num_envs_, rec.data()));
         return rec;
     }
+    void download_into(std::vector<mrsim_env_state>& rec) const {
+        rec.resize(static_cast<std::size_t>(num_envs_));
+        check(mrsim_get_env_states(ctx_, 0, num_envs_, rec.data()));
+    }
     void upload(const std::vector<mrsim_env_state>& rec) {
         check(mrsim_set_env_states(ctx_, 0, static_cast<int64_t>(rec.size()), rec.data()));
     }
+    std::vector<mrsim_env_state>& scratch() { return scratch_; }  // reused per-env records
 
 private:
+    std::vector<mrsim_env_state> scratch_;
     mrsim_cfg cfg_;
     int64_t num_envs_;
     mrsim_ctx* ctx_ = nullptr;
 };
 
 namespace detail {
+// fn(i) for i in [0, n): on the caller's WorkerPool in chunks when one is given.
+template <class F>
+inline void parallel_for(WorkerPool* pool, int64_t n, F&& fn) {
+    if (!pool || pool->size() <= 1 || n < 2048) {
+        for (int64_t i = 0; i < n; ++i) fn(i);
+        return;
+    }
+    const int chunks = pool->size() * 4;
+    const int64_t per = (n + chunks - 1) / chunks;
+    pool->run(chunks, [&](int c) {
+        const int64_t lo = c * per, hi = std::min<int64_t>(n, lo + per);
+        for (int64_t i = lo; i < hi; ++i) fn(i);
+    });
+}
 inline std::vector<std::vector<double>> unpack_obs(const float* o, int n, int d) {
     std::vector<std::vector<double>> out(static_cast<std::size_t>(n), std::vector<double>(static_cast<std::size_t>(d)));
     for (int r = 0; r < n; ++r)
@@ -364,7 +399,8 @@ inline std::vector<std::vector<double>> unpack_obs(const float* o, int n, int d)
 
 /// reset_batch (batch.hpp:240-259) on the device.
 inline std::pair<BatchWorldState, ResetOutput> reset_batch(Engine& eng, const ScenarioConfig& cfg,
-                                                           const std::vector<std::uint64_t>& seeds) {
+                                                           const std::vector<std::uint64_t>& seeds,
+                                                           WorkerPool* pool = nullptr) {
     if (seeds.empty()) throw std::invalid_argument("reset_batch: seed list is empty");
     if (static_cast<int64_t>(seeds.size()) != eng.num_envs())
         throw std::invalid_argument("reset_batch: seed count != engine batch size");
@@ -373,11 +409,14 @@ inline std::pair<BatchWorldState, ResetOutput> reset_batch(Engine& eng, const Sc
     BatchWorldState state;
     ResetOutput out;
     const int n = cfg.num_robots, d = eng.obs_dim();
-    for (const auto& r : rec) state.envs.push_back(from_record(r, cfg));
     std::vector<float> obs(static_cast<std::size_t>(eng.num_envs()) * n * d);
     eng.check(mrsim_observe_host(eng.ctx(), obs.data()));  // device-side assemble_observations
-    for (int64_t e = 0; e < eng.num_envs(); ++e)
-        out.obs.push_back(detail::unpack_obs(obs.data() + static_cast<std::size_t>(e) * n * d, n, d));
+    state.envs.resize(rec.size());
+    out.obs.resize(rec.size());
+    detail::parallel_for(pool, eng.num_envs(), [&](int64_t e) {
+        state.envs[static_cast<std::size_t>(e)] = from_record(rec[static_cast<std::size_t>(e)], cfg);
+        out.obs[static_cast<std::size_t>(e)] = detail::unpack_obs(obs.data() + static_cast<std::size_t>(e) * n * d, n, d);
+    });
     return {std::move(state), std::move(out)};
 }
 
@@ -385,12 +424,15 @@ inline std::pair<BatchWorldState, ResetOutput> reset_batch(Engine& eng, const Sc
 /// batch state is uploaded, stepped with the host actions and downloaded.
 inline std::pair<BatchWorldState, std::vector<StepOutput>> step_batch(Engine& eng, const BatchWorldState& state,
                                                                       const std::vector<int>& actions,
-                                                                      const ScenarioConfig& cfg) {
+                                                                      const ScenarioConfig& cfg,
+                                                                      WorkerPool* pool = nullptr) {
     validate_actions(actions, state.size(), cfg.num_robots);  // reference message and ordering
     if (state.size() != eng.num_envs()) throw std::invalid_argument("step_batch: batch size != engine batch size");
-    std::vector<mrsim_env_state> rec;
-    rec.reserve(state.envs.size());
-    for (const auto& e : state.envs) rec.push_back(to_record(e));
+    std::vector<mrsim_env_state>& rec = eng.scratch();
+    rec.resize(state.envs.size());
+    detail::parallel_for(pool, state.size(), [&](int64_t e) {
+        to_record(state.envs[static_cast<std::size_t>(e)], rec[static_cast<std::size_t>(e)]);
+    });
     eng.upload(rec);
     const int n = cfg.num_robots, d = eng.obs_dim();
     std::vector<float> obs(static_cast<std::size_t>(state.size()) * n * d);
@@ -398,18 +440,57 @@ inline std::pair<BatchWorldState, std::vector<StepOutput>> step_batch(Engine& en
     std::vector<uint8_t> done(static_cast<std::size_t>(state.size()));
     std::vector<int32_t> acts(actions.begin(), actions.end());
     eng.check(mrsim_step_host(eng.ctx(), acts.data(), obs.data(), rew.data(), done.data(), nullptr));
-    auto after = eng.download();
+    eng.download_into(rec);
     BatchWorldState next;
+    next.envs.resize(state.envs.size());
     std::vector<StepOutput> outs(static_cast<std::size_t>(state.size()));
-    for (int e = 0; e < state.size(); ++e) {
-        next.envs.push_back(from_record(after[static_cast<std::size_t>(e)], cfg));
-        StepOutput& o = outs[static_cast<std::size_t>(e)];
-        o.obs = detail::unpack_obs(obs.data() + static_cast<std::size_t>(e) * n * d, n, d);
-        o.team_reward = rew[static_cast<std::size_t>(e)];
-        o.done = done[static_cast<std::size_t>(e)] != 0;
-        o.metrics = next.envs.back().metrics;
-    }
+    detail::parallel_for(pool, state.size(), [&](int64_t e) {
+        const std::size_t k = static_cast<std::size_t>(e);
+        next.envs[k] = from_record(rec[k], cfg);
+        StepOutput& o = outs[k];
+        o.obs = detail::unpack_obs(obs.data() + k * n * d, n, d);
+        o.team_reward = rew[k];
+        o.done = done[k] != 0;
+        o.metrics = next.envs[k].metrics;
+    });
     return {std::move(next), std::move(outs)};
+}
+
+namespace detail {
+// One device context per (flattened config, batch size, device), created on first use.
+inline Engine& cached_engine(const ScenarioConfig& cfg, int64_t num_envs, int device = 0) {
+    static std::mutex mu;
+    static std::map<std::string, std::unique_ptr<Engine>> engines;
+    const mrsim_cfg flat = flatten(cfg);  // zero-initialised, so the bytes are a key
+    std::string key(reinterpret_cast<const char*>(&flat), sizeof flat);
+    key += ":" + std::to_string(num_envs) + ":" + std::to_string(device);
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = engines.find(key);
+    if (it == engines.end()) it = engines.emplace(key, std::make_unique<Engine>(cfg, num_envs, device)).first;
+    return *it->second;
+}
+}  // namespace detail
+
+/// reset_batch with the reference's signature (batch.hpp:240-259): the device context for
+/// (cfg, seeds.size()) is created on first use and cached. `scenario` is resolved on the
+/// device from cfg.scenario_name (Scenario objects are stateless, scenario.hpp:132-134).
+inline std::pair<BatchWorldState, ResetOutput> reset_batch(const ScenarioConfig& cfg,
+                                                           const std::vector<std::uint64_t>& seeds,
+                                                           const Scenario& scenario, WorkerPool* pool = nullptr) {
+    (void)scenario;
+    if (seeds.empty()) throw std::invalid_argument("reset_batch: seed list is empty");
+    return reset_batch(detail::cached_engine(cfg, static_cast<int64_t>(seeds.size())), cfg, seeds, pool);
+}
+
+/// step_batch with the reference's signature (batch.hpp:268-290): pure, same exceptions.
+inline std::pair<BatchWorldState, std::vector<StepOutput>> step_batch(const BatchWorldState& state,
+                                                                      const std::vector<int>& actions,
+                                                                      const ScenarioConfig& cfg,
+                                                                      const Scenario& scenario,
+                                                                      WorkerPool* pool = nullptr) {
+    (void)scenario;
+    validate_actions(actions, state.size(), cfg.num_robots);
+    return step_batch(detail::cached_engine(cfg, state.size()), state, actions, cfg, pool);
 }
 
 /// The device policy used by steps without host actions (Policy / PolicySpec,

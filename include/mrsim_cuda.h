@@ -217,6 +217,9 @@ typedef struct mrsim_ctx mrsim_ctx;
 /* mrsim_create flags */
 #define MRSIM_FLAG_FP64 1u          /* compute in fp64 (default: fp32) */
 #define MRSIM_FLAG_AUTO_RESET 2u    /* reset done envs in-kernel (harness wave semantics) */
+#define MRSIM_FLAG_ENV_PER_THREAD 4u /* teams of <= 4 robots without obstacle rows: step with one thread
+                                       per env instead of the lane-per-robot kernel (same results; measured
+                                       ~25% slower on B200: kept for A/B and tested) */
 
 /* ---- configuration (host only, no device needed) ---- */
 

@@ -577,7 +577,7 @@ int orc_reset_env(const mrsim_cfg* c, uint64_t seed, mrsim_env_state* s, char* e
             }
             break;
         }
-        case MRSIM_TASK_PREDATOR_PREY: { /* predator_prey.hpp:157-175 */
+        case MRSIM_TASK_PREDATOR_PREY: { /* predator_prey.hpp:48-66 */
             int placed = 0;
             for (int attempt = 0; attempt < 1000 && !placed; ++attempt) {
                 double px = uniform(&rng, -hw + sm, hw - sm);
@@ -594,7 +594,7 @@ int orc_reset_env(const mrsim_cfg* c, uint64_t seed, mrsim_env_state* s, char* e
             if (!placed) return fail(err, errlen, MRSIM_E_RUNTIME, "predator_prey: could not place prey");
             break;
         }
-        case MRSIM_TASK_DISCOVERY: { /* discovery.hpp:243-254 */
+        case MRSIM_TASK_DISCOVERY: { /* discovery.hpp:27-38 */
             const double lm = y->discovery_landmark_margin;
             s->num_landmarks = y->discovery_num_landmarks;
             for (int k = 0; k < s->num_landmarks; ++k) {
@@ -617,7 +617,7 @@ int orc_reset_env(const mrsim_cfg* c, uint64_t seed, mrsim_env_state* s, char* e
             }
             break;
         }
-        case MRSIM_TASK_FORAGING: { /* foraging.hpp:190-212 */
+        case MRSIM_TASK_FORAGING: { /* foraging.hpp:27-49 */
             double l0 = -INFINITY, l1 = -INFINITY;
             for (int i = 0; i < c->het_rows; ++i) {
                 double v = c->het[i][0];
@@ -643,7 +643,7 @@ int orc_reset_env(const mrsim_cfg* c, uint64_t seed, mrsim_env_state* s, char* e
             s->total_initial = s->circle_remaining + s->rect_remaining;
             break;
         }
-        case MRSIM_TASK_ARCTIC_TRANSPORT: { /* arctic_transport.hpp:127-142 */
+        case MRSIM_TASK_ARCTIC_TRANSPORT: { /* arctic_transport.hpp:30-45 */
             s->cols = y->arctic_grid_cols;
             s->rows = y->arctic_grid_rows;
             memcpy(s->goal_zone, y->arctic_goal_zone, sizeof s->goal_zone);
@@ -680,12 +680,12 @@ static double transition(const mrsim_cfg* c, mrsim_env_state* s, rng_t* rng) {
             }
             return 0.0;
         }
-        case MRSIM_TASK_NAVIGATION: { /* navigation.hpp:77-83 */
+        case MRSIM_TASK_NAVIGATION: { /* navigation.hpp:45-51 */
             double total = 0.0;
             for (int i = 0; i < N; ++i) total += hypot(s->x[i] - s->goals[i][0], s->y[i] - s->goals[i][1]);
             return c->coef[MRSIM_COEF_DIST] * total;
         }
-        case MRSIM_TASK_PREDATOR_PREY: { /* predator_prey.hpp:121-143, 177-199 */
+        case MRSIM_TASK_PREDATOR_PREY: { /* predator_prey.hpp:15-34, 177-199 */
             double robot_step = 0.0;
             for (int i = 0; i < N; ++i) robot_step = dmax(robot_step, c->step_sizes[i]);
             double step = y->pp_prey_agility * robot_step;
@@ -720,7 +720,7 @@ static double transition(const mrsim_cfg* c, mrsim_env_state* s, rng_t* rng) {
             }
             return tagged ? c->coef[MRSIM_COEF_TAG] : 0.0;
         }
-        case MRSIM_TASK_DISCOVERY: { /* discovery.hpp:256-283 */
+        case MRSIM_TASK_DISCOVERY: { /* discovery.hpp:40-69 */
             int ns = 0, nt = 0;
             for (int k = 0; k < s->num_landmarks; ++k) {
                 if (s->tagged[k]) continue;
@@ -785,7 +785,7 @@ static double transition(const mrsim_cfg* c, mrsim_env_state* s, rng_t* rng) {
             }
             return reward;
         }
-        case MRSIM_TASK_FORAGING: { /* foraging.hpp:214-231 */
+        case MRSIM_TASK_FORAGING: { /* foraging.hpp:51-70 */
             double reward = 0.0;
             for (int r = 0; r < s->num_resources; ++r) {
                 if (s->foraged[r]) continue;
@@ -865,7 +865,7 @@ static double transition(const mrsim_cfg* c, mrsim_env_state* s, rng_t* rng) {
 }
 
 static void finalize(const mrsim_cfg* c, mrsim_env_state* s) {
-    if (c->task == MRSIM_TASK_NAVIGATION) { /* navigation.hpp:85-93 */
+    if (c->task == MRSIM_TASK_NAVIGATION) { /* navigation.hpp:53-61 */
         int all = 1;
         for (int i = 0; i < c->num_robots; ++i)
             all = all && hypot(s->x[i] - s->goals[i][0], s->y[i] - s->goals[i][1]) <= c->layout.navigation_on_goal_radius;
@@ -894,7 +894,7 @@ int orc_observe(const mrsim_cfg* c, const mrsim_env_state* s, double* obs) {
             o[q++] = s->theta[r];
             o[q++] = s->targets[r][0];
             o[q++] = s->targets[r][1];
-        } else if (c->task == MRSIM_TASK_NAVIGATION) { /* navigation.hpp:96-102 */
+        } else if (c->task == MRSIM_TASK_NAVIGATION) { /* navigation.hpp:64-70 */
             o[q++] = s->x[r];
             o[q++] = s->y[r];
             o[q++] = s->theta[r];

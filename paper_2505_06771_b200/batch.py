@@ -151,7 +151,7 @@ class CudaEnvBatch:
     """B environments stepped in lockstep on one GPU (one mrsim_ctx)."""
 
     def __init__(self, cfg: ScenarioConfig, num_envs: int, device: int = 0, fp64: bool = True,
-                 auto_reset: bool = False):
+                 auto_reset: bool = False, env_per_thread: bool = False):
         cfg.validate()
         self.cfg = cfg.copy()
         self.num_envs = int(num_envs)
@@ -160,7 +160,8 @@ class CudaEnvBatch:
         self.auto_reset = bool(auto_reset)
         self.N = cfg.raw.num_robots
         self.D = cfg.obs_dim
-        flags = (_abi.MRSIM_FLAG_FP64 if fp64 else 0) | (_abi.MRSIM_FLAG_AUTO_RESET if auto_reset else 0)
+        flags = (_abi.MRSIM_FLAG_FP64 if fp64 else 0) | (_abi.MRSIM_FLAG_AUTO_RESET if auto_reset else 0) | \
+            (_abi.MRSIM_FLAG_ENV_PER_THREAD if env_per_thread else 0)
         handle = ctypes.c_void_p()
         rc = lib().mrsim_create(ctypes.byref(self.cfg.raw), self.device, self.num_envs, flags,
                                 ctypes.byref(handle))

@@ -37,7 +37,6 @@ struct mrsim_ctx {
     long long scripted_launches = 0;
     int cur = 0;
     long long serial = 0;
-    int hist_in[64] = {0};
     bool has_episodes = false;
     uint64_t root_seed = 0;
     long long episode_stride = 0;
@@ -66,6 +65,22 @@ struct mrsim_ctx {
     mrsim_traj_record* d_cap = nullptr;
     long long cap_max = 0, cap_steps = 0;
 };
+
+namespace mrsim_dev {
+__global__ void stats_rollback_kernel(EnvStats st, long long serial, long long B) {
+    const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= B || st.upd_serial[e] != serial) return;
+    st.episodes[e] = st.u_episodes[e];
+    st.ret[e] = st.u_ret[e];
+    st.ret_sq[e] = st.u_ret_sq[e];
+    st.metric[e] = st.u_metric[e];
+    st.success[e] = st.u_success[e];
+    st.min_dist[e] = st.u_min_dist[e];
+    st.collisions[e] = st.u_collisions[e];
+    st.qp_inf[e] = st.u_qp_inf[e];
+    st.upd_serial[e] = -1;
+}
+}  // namespace mrsim_dev
 
 namespace {
 
@@ -219,8 +234,11 @@ cudaError_t scripted_launch(mrsim_ctx* ctx, const DevState<Real>& st, int8_t* ou
     mrsim_dev::prey_offsets(ctx->cfg, p.prey_off);
     p.actions = out;
     p.ticket = ctx->d_ticket + 2;
-    p.serial = ctx->scripted_launches++;
-    return dispatch_scripted<Real>(ctx->cfg.task, p, s);
+    p.serial = ctx->scripted_launches;
+    p.num_sms = ctx->num_sms;
+    const cudaError_t e = dispatch_scripted<Real>(ctx->cfg.task, p, s);
+    if (e == cudaSuccess) ++ctx->scripted_launches;  // the next launch clears the counter this one used
+    return e;
 }
 
 template <class Real>
@@ -242,6 +260,7 @@ cudaError_t policy_launch(mrsim_ctx* ctx, const DevState<Real>& st, int8_t* out,
     for (int l = 0; l < ctx->net.num_layers; ++l) maxw = maxw > ctx->net.out[l] ? maxw : ctx->net.out[l];
     p.maxw = maxw;
     p.warp_bytes = mrsim_dev::policy_warp_bytes<Real>(ctx->N, maxw);
+    p.num_sms = ctx->num_sms;
     p.actions = out;
     return dispatch_policy<Real>(ctx->cfg.task, p, s);
 }
@@ -303,7 +322,7 @@ int check_device_error(mrsim_ctx* ctx, bool rollback, const int32_t* host_action
     const unsigned code = static_cast<unsigned>(w & 0xff);
     const int detail = static_cast<int>((w >> 8) & 0xff);
     const int robot = static_cast<int>((w >> 16) & 0xff);
-    const long long env = static_cast<long long>(w >> 24);
+    const long long env = static_cast<long long>((w >> 24) & ((1ull << mrsim_dev::kErrEnvBits) - 1));
     char buf[256];
     if (code == mrsim_dev::kErrInvalidAction)  // the device keeps 8 bits; the host buffer has the full value
         std::snprintf(buf, sizeof buf, "step_batch: invalid action %d for environment %lld, robot %d",
@@ -314,8 +333,14 @@ int check_device_error(mrsim_ctx* ctx, bool rollback, const int32_t* host_action
                       robot, env);
     else
         std::snprintf(buf, sizeof buf, "%s (environment %lld, robot %d)", err_text(code), env, robot);
-    if (rollback && ser >= 0 && ser < ctx->serial && ctx->serial - ser <= 64) {
-        ctx->cur = ctx->hist_in[ser % 64];  // state as it was before the failing step
+    if (rollback && ser >= 0 && ser < ctx->serial) {
+        // Every launched step flips the ping-pong index once and the steps after the failing
+        // one are no-ops, so the failing step's (untouched) input buffer is the current one
+        // flipped by the parity of the number of steps launched since.
+        ctx->cur ^= static_cast<int>((ctx->serial - ser) & 1);
+        const unsigned grid = static_cast<unsigned>((ctx->B + 255) / 256);
+        mrsim_dev::stats_rollback_kernel<<<grid, 256>>>(ctx->st, ser, ctx->B);  // and its episode stats
+        cudaDeviceSynchronize();
     }
     // clear so the context stays usable after the caller handled the error
     const unsigned long long none = ~0ull;
@@ -365,7 +390,6 @@ StepParams<Real> step_params(mrsim_ctx* ctx, DevState<Real>* s, const int8_t* ac
 
 // Bookkeeping after every env of a step has been launched (ping-pong flip, rollback history).
 void step_done(mrsim_ctx* ctx) {
-    ctx->hist_in[ctx->serial % 64] = ctx->cur;
     ctx->serial += 1;
     ctx->cur = 1 - ctx->cur;
     ctx->env_steps += ctx->B;
@@ -378,7 +402,7 @@ int do_step(mrsim_ctx* ctx, DevState<Real>* s, const int8_t* actions, float* obs
     StepParams<Real> p = step_params<Real>(ctx, s, actions, obs, reward, done, next_obs, reward64, actions32);
     // warp-staged obs stores only where they pay: obs going straight to pinned host memory
     // (device-memory obs: ~2 % slower staged, measured)
-    p.obs_stage = stage_obs ? ctx->obs_stage : 0;
+    p.obs_stage = (stage_obs || ctx->L == 1) ? ctx->obs_stage : 0;
     const int smem = ctx->smem_group * (ctx->block / ctx->L) + 4 * p.obs_stage * (ctx->block / 32);
     cudaError_t e = dispatch_step<Real>(ctx->cfg.task, p, ctx->var, ctx->grid, ctx->block, smem, stream);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "step kernel launch");
@@ -737,7 +761,7 @@ int mrsim_create(const mrsim_cfg* cfg, int device, int64_t num_envs, uint32_t fl
     ctx->D = mrsim_dev::obs_dim_of(*cfg);
     ctx->bdim = mrsim_dev::base_obs_dim(*cfg);
     mrsim_dev::task_fields(*cfg, &ctx->nf, &ctx->ni);
-    ctx->var = mrsim_host::pick_variant(*cfg);  // lane per robot
+    ctx->var = mrsim_host::pick_variant(*cfg, flags);  // thread per env (N <= 4) or lane per robot
     ctx->L = ctx->var.L;
     cudaError_t e = cudaSetDevice(device);
     if (e != cudaSuccess) {
@@ -761,7 +785,9 @@ int mrsim_create(const mrsim_cfg* cfg, int device, int64_t num_envs, uint32_t fl
         if (ctx->fp64) carve_state(ctx->mem[k], ctx->B, ctx->N, ctx->nf, ctx->ni, ctx->sd[k]);
         else carve_state(ctx->mem[k], ctx->B, ctx->N, ctx->nf, ctx->ni, ctx->sf[k]);
     }
-    const size_t stb = static_cast<size_t>(ctx->B) * (4 + 8 * 5 + 8 * 2) + 8 * 256;
+    // stats + undo log (values before the last update) + update serial; 256-byte aligned arrays
+    const size_t stb = 2 * (static_cast<size_t>(ctx->B) * (4 + 8 * 5 + 8 * 2) + 8 * 256) +
+                       static_cast<size_t>(ctx->B) * 8 + 256;
     if ((e = cudaMalloc(&ctx->stats_mem, stb)) != cudaSuccess) return bail(e, "cudaMalloc stats");
     {
         char* p = static_cast<char*>(ctx->stats_mem);
@@ -770,17 +796,28 @@ int mrsim_create(const mrsim_cfg* cfg, int device, int64_t num_envs, uint32_t fl
             p += (bytes + 255) & ~size_t(255);
             return r;
         };
-        ctx->st.episodes = reinterpret_cast<int32_t*>(take(4 * ctx->B));
-        ctx->st.ret = reinterpret_cast<double*>(take(8 * ctx->B));
-        ctx->st.ret_sq = reinterpret_cast<double*>(take(8 * ctx->B));
-        ctx->st.metric = reinterpret_cast<double*>(take(8 * ctx->B));
-        ctx->st.success = reinterpret_cast<double*>(take(8 * ctx->B));
-        ctx->st.min_dist = reinterpret_cast<double*>(take(8 * ctx->B));
-        ctx->st.collisions = reinterpret_cast<int64_t*>(take(8 * ctx->B));
-        ctx->st.qp_inf = reinterpret_cast<int64_t*>(take(8 * ctx->B));
+        mrsim_dev::EnvStats& st = ctx->st;
+        st.episodes = reinterpret_cast<int32_t*>(take(4 * ctx->B));
+        st.ret = reinterpret_cast<double*>(take(8 * ctx->B));
+        st.ret_sq = reinterpret_cast<double*>(take(8 * ctx->B));
+        st.metric = reinterpret_cast<double*>(take(8 * ctx->B));
+        st.success = reinterpret_cast<double*>(take(8 * ctx->B));
+        st.min_dist = reinterpret_cast<double*>(take(8 * ctx->B));
+        st.collisions = reinterpret_cast<int64_t*>(take(8 * ctx->B));
+        st.qp_inf = reinterpret_cast<int64_t*>(take(8 * ctx->B));
+        st.u_episodes = reinterpret_cast<int32_t*>(take(4 * ctx->B));
+        st.u_ret = reinterpret_cast<double*>(take(8 * ctx->B));
+        st.u_ret_sq = reinterpret_cast<double*>(take(8 * ctx->B));
+        st.u_metric = reinterpret_cast<double*>(take(8 * ctx->B));
+        st.u_success = reinterpret_cast<double*>(take(8 * ctx->B));
+        st.u_min_dist = reinterpret_cast<double*>(take(8 * ctx->B));
+        st.u_collisions = reinterpret_cast<int64_t*>(take(8 * ctx->B));
+        st.u_qp_inf = reinterpret_cast<int64_t*>(take(8 * ctx->B));
+        st.upd_serial = reinterpret_cast<long long*>(take(8 * ctx->B));
         cudaMemset(ctx->stats_mem, 0, stb);
+        cudaMemset(st.upd_serial, 0xff, 8 * ctx->B);  // -1: no update yet
         std::vector<double> inf(ctx->B, INFINITY);
-        cudaMemcpy(ctx->st.min_dist, inf.data(), 8 * ctx->B, cudaMemcpyHostToDevice);
+        cudaMemcpy(st.min_dist, inf.data(), 8 * ctx->B, cudaMemcpyHostToDevice);
     }
     // error word, its step serial, then the step kernel's two warp-task counters
     if ((e = cudaMalloc(&ctx->d_err, 32)) != cudaSuccess) return bail(e, "cudaMalloc err");
@@ -790,6 +827,21 @@ int mrsim_create(const mrsim_cfg* cfg, int device, int64_t num_envs, uint32_t fl
     const unsigned long long none = ~0ull;
     cudaMemcpy(ctx->d_err, &none, sizeof none, cudaMemcpyHostToDevice);
     cudaMemset(ctx->d_err_serial, 0xff, 8);
+    if (ctx->L == 1) {  // one thread per env: a plain grid of 64-env blocks, obs staged per warp
+        ctx->block = mrsim_dev::kEnvBlock;
+        const int stage = 32 * ctx->N * ctx->D;
+        ctx->obs_stage = stage <= mrsim_dev::kEnvObsStageMax ? stage : 0;
+        ctx->smem_group = 0;
+        ctx->grid = static_cast<int>((ctx->B + ctx->block - 1) / ctx->block);
+        int bps = 0;
+        const int smem = 4 * ctx->obs_stage * (ctx->block / 32);
+        e = ctx->fp64 ? dispatch_occ<double>(cfg->task, ctx->var, ctx->block, smem, &bps)
+                      : dispatch_occ<float>(cfg->task, ctx->var, ctx->block, smem, &bps);
+        if (e != cudaSuccess) return bail(e, "occupancy query");
+        if ((e = cudaDeviceSynchronize()) != cudaSuccess) return bail(e, "create sync");
+        *out = ctx;
+        return MRSIM_OK;
+    }
     // launch geometry: persistent grid of (SMs x resident blocks)
     ctx->smem_group =
         ctx->fp64 ? mrsim_dev::GroupSmem<double>::bytes(ctx->N, ctx->nf, ctx->ni, ctx->var.L, ctx->var.MP, ctx->var.MO)

@@ -234,12 +234,12 @@ int mrsim_config_default(const char* scenario, mrsim_cfg* out) {
             c.max_steps = 100;
             set_coef(&c, MRSIM_COEF_DIST, -1.0);
             break;
-        case MRSIM_TASK_PREDATOR_PREY:  // predator_prey.hpp:149-155
+        case MRSIM_TASK_PREDATOR_PREY:  // predator_prey.hpp:40-46
             steps(3, 0.2);
             c.max_steps = 100;
             set_coef(&c, MRSIM_COEF_TAG, 10.0);
             break;
-        case MRSIM_TASK_DISCOVERY: {  // discovery.hpp:232-241
+        case MRSIM_TASK_DISCOVERY: {  // discovery.hpp:16-25
             steps(4, 0.2);
             c.max_steps = 100;
             const double v[] = {0.45, 0, 0.45, 0, 0, 0.25, 0, 0.25};
@@ -254,7 +254,7 @@ int mrsim_config_default(const char* scenario, mrsim_cfg* out) {
             c.max_steps = 100;
             set_coef(&c, MRSIM_COEF_DROPOFF, 1.0);
             break;
-        case MRSIM_TASK_FORAGING: {  // foraging.hpp:178-186
+        case MRSIM_TASK_FORAGING: {  // foraging.hpp:15-25
             steps(3, 0.2);
             c.max_steps = 100;
             const double v[] = {1, 2, 3};
@@ -282,7 +282,7 @@ int mrsim_config_default(const char* scenario, mrsim_cfg* out) {
             set_coef(&c, MRSIM_COEF_STEP, -0.10);
             break;
         }
-        case MRSIM_TASK_WAREHOUSE: {  // warehouse.hpp:241-250
+        case MRSIM_TASK_WAREHOUSE: {  // warehouse.hpp:14-23
             steps(4, 0.2);
             c.max_steps = 70;
             const double v[] = {1, 0, 1, 0, 0, 1, 0, 1};

@@ -6,6 +6,7 @@
 
 #include "policy.cuh"
 #include "scripted.cuh"
+#include "env_kernel.cuh"
 #include "step_kernel.cuh"
 
 namespace mrsim_host {
@@ -44,13 +45,21 @@ inline void fill_consts(const mrsim_cfg& c, mrsim_dev::PhysConsts<Real>& k) {
 }
 
 // Kernel variant for a config: L lanes per env (lane per robot), MP pair-row
-// slots per lane, MO obstacle-row slots per lane (rware only).
+// slots per lane, MO obstacle-row slots per lane (rware only); L = 1 is the
+// one-thread-per-env kernel (env_kernel.cuh) for teams of <= 4 robots without
+// obstacle rows, on request (MRSIM_FLAG_ENV_PER_THREAD).
 struct Variant {
     int L, MP, MO;
 };
-inline Variant pick_variant(const mrsim_cfg& c) {
+inline Variant pick_variant(const mrsim_cfg& c, unsigned flags = 0) {
     const int N = c.num_robots, P = N * (N - 1) / 2;
     Variant v;
+    if (N <= mrsim_dev::kEnvNR && c.task != MRSIM_TASK_RWARE && (flags & MRSIM_FLAG_ENV_PER_THREAD)) {
+        v.L = 1;
+        v.MP = 0;
+        v.MO = 0;
+        return v;
+    }
     v.L = N <= 4 ? 4 : (N <= 8 ? 8 : 16);
     const int need = (P + v.L - 1) / v.L;
     if (v.L == 4) v.MP = 2;

@@ -133,9 +133,12 @@ __host__ __device__ __forceinline__ uint64_t policy_key_of(uint64_t seed) {
 }
 
 // ---------------------------------------------------------------------------
-// Device error word: the first (lowest env) error wins, mirroring the
-// reference's sequential validation order (batch.hpp:226-237).
-// code layout: [env:40][robot:8][code:8] in a u64 for atomicMin.
+// Device error word, ordered like the reference's step_batch: validate_actions
+// checks every env's actions before any env is stepped (batch.hpp:226-237,
+// 271), so an invalid action anywhere outranks a physics/spawn error in any
+// env; within a class the lowest env wins (the sequential order).
+// Layout (u64, atomicMin): [class:1][env:39][robot:8][detail:8][code:8],
+// class 0 = invalid action, 1 = every other error.
 // ---------------------------------------------------------------------------
 enum DevErr : unsigned {
     kErrInvalidAction = 1,   // invalid_argument: step_batch: invalid action
@@ -145,9 +148,12 @@ enum DevErr : unsigned {
     kErrGoals = 5,           // runtime_error: navigation could not place goals
     kErrPrey = 6,            // runtime_error: predator_prey could not place prey
 };
+constexpr int kErrEnvBits = 39;
 __device__ __forceinline__ void report_error(unsigned long long* err, long long env, int robot, unsigned code,
                                              int detail = 0) {
-    unsigned long long v = (static_cast<unsigned long long>(env) << 24) |
+    const unsigned long long cls = code == kErrInvalidAction ? 0ull : 1ull;
+    unsigned long long v = (cls << 63) |
+                           ((static_cast<unsigned long long>(env) & ((1ull << kErrEnvBits) - 1)) << 24) |
                            (static_cast<unsigned long long>(robot & 0xff) << 16) |
                            (static_cast<unsigned long long>(detail & 0xff) << 8) | (code & 0xff);
     atomicMin(err, v);

@@ -44,6 +44,7 @@ struct PolicyParams {
     const double* wT;  // per layer [in][out]
     const double* bias;
     PolicyNet net;
+    int num_sms;       // of the context's device (grid sizing)
     int8_t* actions;   // [B][N]
 };
 

@@ -394,6 +394,7 @@ struct ScriptedParams {
     unsigned* ticket;  // [2] env counters, used by alternate launches (serial & 1)
     long long serial;  // launch count of this context's scripted kernel
     int smem_stride;   // bytes of shared memory per warp (scripted_smem_stride)
+    int num_sms;       // of the context's device (grid sizing)
 };
 
 template <class Real, int TASK>

@@ -35,6 +35,17 @@ static cudaError_t occ_V(int block, int smem, int* bps) {
 template <class Real>
 static cudaError_t launch_any(const mrsim_dev::StepParams<Real>& p, Variant v, int grid, int block, int smem,
                               cudaStream_t s) {
+    if constexpr (MRSIM_TASK_ID != MRSIM_TASK_RWARE) {
+        if (v.L == 1) {  // one thread per env (env_kernel.cuh)
+            auto k = mrsim_dev::env_step_kernel<Real, MRSIM_TASK_ID>;
+            if (smem + mrsim_dev::kEnvStaticSmem > 46 * 1024) {  // dynamic obs stage + static row/pose tables
+                cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                if (e != cudaSuccess) return e;
+            }
+            k<<<grid, block, smem, s>>>(p);
+            return cudaGetLastError();
+        }
+    }
 #define MRSIM_CASE(l, mp, mo) \
     if (v.L == l && v.MP == mp && v.MO == mo) return launch_V<Real, l, mp, mo>(p, grid, block, smem, s);
     if constexpr (MRSIM_TASK_ID == MRSIM_TASK_RWARE) {
@@ -49,6 +60,16 @@ static cudaError_t launch_any(const mrsim_dev::StepParams<Real>& p, Variant v, i
 
 template <class Real>
 static cudaError_t occ_any(Variant v, int block, int smem, int* bps) {
+    if constexpr (MRSIM_TASK_ID != MRSIM_TASK_RWARE) {
+        if (v.L == 1) {
+            auto k = mrsim_dev::env_step_kernel<Real, MRSIM_TASK_ID>;
+            if (smem + mrsim_dev::kEnvStaticSmem > 46 * 1024) {
+                cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                if (e != cudaSuccess) return e;
+            }
+            return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k, block, smem);
+        }
+    }
 #define MRSIM_CASE(l, mp, mo) \
     if (v.L == l && v.MP == mp && v.MO == mo) return occ_V<Real, l, mp, mo>(block, smem, bps);
     if constexpr (MRSIM_TASK_ID == MRSIM_TASK_RWARE) {
@@ -116,13 +137,18 @@ static cudaError_t launch_policy_any(const mrsim_dev::PolicyParams<Real>& p, cud
     int warps = mrsim_dev::kPolicyWarps;  // fewer warps per block when one env's buffers are large
     while (warps > 1 && warps * p.warp_bytes > 200 * 1024) warps >>= 1;
     const long long want = (p.B + warps - 1) / warps;
-    const unsigned grid = static_cast<unsigned>(want < 148 * 64 ? want : 148 * 64);
     const int smem = warps * p.warp_bytes;
     auto k = mrsim_dev::policy_kernel<Real, MRSIM_TASK_ID>;
     if (smem > 48 * 1024) {
         const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
     }
+    // grid-stride over envs: one full wave of resident blocks on this device
+    int bps = 0;
+    cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, 32 * warps, smem);
+    if (oe != cudaSuccess) return oe;
+    const long long full = static_cast<long long>(p.num_sms) * (bps > 0 ? bps : 1);
+    const unsigned grid = static_cast<unsigned>(want < full ? want : full);
     k<<<grid, 32 * warps, smem, s>>>(p);
     return cudaGetLastError();
 }
@@ -138,7 +164,6 @@ cudaError_t launch_policy<double, MRSIM_TASK_ID>(const mrsim_dev::PolicyParams<d
 template <class Real>
 static cudaError_t launch_scripted_any(const mrsim_dev::ScriptedParams<Real>& p, cudaStream_t s) {
     const long long want = (p.B + mrsim_dev::kPolicyWarps - 1) / mrsim_dev::kPolicyWarps;
-    const unsigned grid = static_cast<unsigned>(want < 148 * 16 ? want : 148 * 16);
     // grid cells as mrsim_set_policy_scripted sizes them (0.05 m, policy.hpp:253-255)
     const int cols = static_cast<int>((2.0 * p.c.arena_half_width) / 0.05);
     const int rows = static_cast<int>((2.0 * p.c.arena_half_height) / 0.05);
@@ -150,6 +175,12 @@ static cudaError_t launch_scripted_any(const mrsim_dev::ScriptedParams<Real>& p,
         const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
     }
+    // persistent: one full wave of resident blocks on this device (warps take envs from a counter)
+    int bps = 0;
+    cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, 32 * mrsim_dev::kPolicyWarps, smem);
+    if (oe != cudaSuccess) return oe;
+    const long long full = static_cast<long long>(p.num_sms) * (bps > 0 ? bps : 1);
+    const unsigned grid = static_cast<unsigned>(want < full ? want : full);
     k<<<grid, 32 * mrsim_dev::kPolicyWarps, smem, s>>>(q);
     return cudaGetLastError();
 }

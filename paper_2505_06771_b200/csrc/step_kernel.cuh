@@ -49,12 +49,45 @@ struct DevState {
     int32_t* ti;                               // [ni][B]
 };
 
-// Per-env accumulators over completed episodes (single buffer).
+// Per-env accumulators over completed episodes (single buffer, touched only on
+// done steps), with a one-level undo log: a step that fails is rolled back by
+// the host (step_batch is pure, batch.hpp:267), and so are the stats it had
+// already accumulated for other envs (stats_rollback_kernel).
 struct EnvStats {
     int32_t* episodes;
     double *ret, *ret_sq, *metric, *success, *min_dist;
     int64_t *collisions, *qp_inf;
+    int32_t* u_episodes;  // undo log: the values before the last update, and its step serial
+    double *u_ret, *u_ret_sq, *u_metric, *u_success, *u_min_dist;
+    int64_t *u_collisions, *u_qp_inf;
+    long long* upd_serial;
 };
+
+// EpisodeStats update of a finished episode (harness.hpp:277-285).
+__device__ __forceinline__ void stats_commit(const EnvStats& st, long long e, long long serial, double ret,
+                                             double metric, int success, int collisions, int qp_inf,
+                                             double min_dist) {
+    st.u_episodes[e] = st.episodes[e];
+    st.u_ret[e] = st.ret[e];
+    st.u_ret_sq[e] = st.ret_sq[e];
+    st.u_metric[e] = st.metric[e];
+    st.u_success[e] = st.success[e];
+    st.u_min_dist[e] = st.min_dist[e];
+    st.u_collisions[e] = st.collisions[e];
+    st.u_qp_inf[e] = st.qp_inf[e];
+    st.upd_serial[e] = serial;
+    st.episodes[e] += 1;
+    st.ret[e] += ret;
+    st.ret_sq[e] += ret * ret;
+    st.metric[e] += metric;
+    st.success[e] += success ? 1.0 : 0.0;
+    st.collisions[e] += collisions;
+    st.qp_inf[e] += qp_inf;
+    st.min_dist[e] = fmin(st.min_dist[e], min_dist);
+}
+
+// Undo the stats updates of the failed step `serial`.
+__global__ void stats_rollback_kernel(EnvStats st, long long serial, long long B);
 
 // Derived constants: SimParams, gains, BarrierConfig with the projection
 // inflation of apply_barrier (barrier.hpp:151-157, 173).
@@ -440,10 +473,16 @@ struct GroupSmem {
 
 // wrap_angle (core.hpp:102-108) for |t| < 3*pi: remainder(t, 2*pi) is t -/+ 2*pi,
 // exact by Sterbenz, so this is bit-identical to the reference on the tick path.
+// The far branch (|t| >= 3*pi: never reached from a tick, where |omega*dt| <= 0.12)
+// is an out-of-line call so the inlined remainder() does not bloat the tick loops.
+template <class Real>
+__device__ __noinline__ Real wrap_angle_far(Real t) {
+    return remainder(t, Consts<Real>::two_pi);
+}
 template <class Real>
 __device__ __forceinline__ Real wrap_angle_dev(Real t) {
     Real r = t;
-    if (dabs(r) >= Real(3) * Consts<Real>::pi) r = remainder(t, Consts<Real>::two_pi);
+    if (dabs(r) >= Real(3) * Consts<Real>::pi) r = wrap_angle_far(t);
     else if (r > Consts<Real>::pi) r -= Consts<Real>::two_pi;
     else if (r < -Consts<Real>::pi) r += Consts<Real>::two_pi;
     if (r <= -Consts<Real>::pi) r += Consts<Real>::two_pi;
@@ -726,16 +765,9 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
                 if (p.reward) p.reward[e] = static_cast<float>(reward);
                 if (p.reward64) p.reward64[e] = static_cast<double>(reward);
                 if (p.done) p.done[e] = static_cast<uint8_t>(done);
-                if (done && new_step == c.max_steps) {  // EpisodeStats (harness.hpp:277-285)
-                    p.st.episodes[e] += 1;
-                    p.st.ret[e] += static_cast<double>(ep_return);
-                    p.st.ret_sq[e] += static_cast<double>(ep_return) * static_cast<double>(ep_return);
-                    p.st.metric[e] += static_cast<double>(metric);
-                    p.st.success[e] += success ? 1.0 : 0.0;
-                    p.st.collisions[e] += collisions;
-                    p.st.qp_inf[e] += qp_inf;
-                    p.st.min_dist[e] = fmin(p.st.min_dist[e], static_cast<double>(min_dist));
-                }
+                if (done && new_step == c.max_steps)  // EpisodeStats (harness.hpp:277-285)
+                    stats_commit(p.st, e, p.serial, static_cast<double>(ep_return), static_cast<double>(metric),
+                                 success, collisions, qp_inf, static_cast<double>(min_dist));
                 p.out.step_index[e] = new_step;
                 p.out.collisions[e] = collisions;
                 p.out.qp_inf[e] = qp_inf;

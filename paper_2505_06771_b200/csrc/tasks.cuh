@@ -156,7 +156,7 @@ __device__ inline int reset_task(const mrsim_cfg& c, uint64_t key, ResetOut& o, 
             }
             if (!placed) { *bad = i; return kErrGoals; }
         }
-    } else if (TASK == MRSIM_TASK_PREDATOR_PREY) {  // predator_prey.hpp:157-175
+    } else if (TASK == MRSIM_TASK_PREDATOR_PREY) {  // predator_prey.hpp:48-66
         const double xmin = -hw + sm, xmax = hw - sm, ymin = -hh + sm, ymax = hh - sm;
         bool placed = false;
         for (int attempt = 0; attempt < 1000 && !placed; ++attempt) {
@@ -173,7 +173,7 @@ __device__ inline int reset_task(const mrsim_cfg& c, uint64_t key, ResetOut& o, 
         }
         if (!placed) { *bad = 0; return kErrPrey; }
         o.ti[0] = 0;  // flash_timer
-    } else if (TASK == MRSIM_TASK_DISCOVERY) {  // discovery.hpp:243-254
+    } else if (TASK == MRSIM_TASK_DISCOVERY) {  // discovery.hpp:27-38
         const double lm = y.discovery_landmark_margin;
         for (int k = 0; k < y.discovery_num_landmarks; ++k) {
             o.tf[2 * k] = rng.uniform(-hw + lm, hw - lm);
@@ -196,7 +196,7 @@ __device__ inline int reset_task(const mrsim_cfg& c, uint64_t key, ResetOut& o, 
             for (int q = idx; q < np - 1; ++q) pool[q] = pool[q + 1];
             --np;
         }
-    } else if (TASK == MRSIM_TASK_FORAGING) {  // foraging.hpp:190-212
+    } else if (TASK == MRSIM_TASK_FORAGING) {  // foraging.hpp:27-49
         double l0 = -1e300, l1 = -1e300;  // two highest robot levels
         for (int i = 0; i < c.het_rows; ++i) {
             const double v = c.het[i][0];
@@ -224,7 +224,7 @@ __device__ inline int reset_task(const mrsim_cfg& c, uint64_t key, ResetOut& o, 
         o.tf[2] = 0.0;            // delivered
         o.tf[3] = circle + rect;  // total_initial
         for (int i = 0; i < N; ++i) o.tf[4 + i] = 0.0;
-    } else if (TASK == MRSIM_TASK_ARCTIC_TRANSPORT) {  // arctic_transport.hpp:127-142
+    } else if (TASK == MRSIM_TASK_ARCTIC_TRANSPORT) {  // arctic_transport.hpp:30-45
         const int cols = y.arctic_grid_cols, rows = y.arctic_grid_rows;
         for (int t = 0; t < cols * rows; ++t) ti_set_byte(o.ti, t, 0);
         for (int r = 0; r < rows; ++r)
@@ -257,7 +257,7 @@ struct EnvView {
 };
 
 // arctic: the grid cell under a robot, with the observation's truncating casts
-// (arctic_transport.hpp:206-209); used per drone for its 3x3 patch.
+// (arctic_transport.hpp:108-112); used per drone for its 3x3 patch.
 template <class Real>
 __device__ __forceinline__ void arctic_cell(const mrsim_cfg& c, Real x, Real y, int& c0, int& r0) {
     const int cols = c.layout.arctic_grid_cols, rows = c.layout.arctic_grid_rows;
@@ -268,8 +268,8 @@ __device__ __forceinline__ void arctic_cell(const mrsim_cfg& c, Real x, Real y, 
     r0 = static_cast<int>(dclamp((y - (-hh)) / ch, Real(0), Real(rows - 1)));
 }
 
-// predator_prey: prey_step = agility * max step size (predator_prey.hpp:177-181) and the
-// 8 compass offsets Vec2{cos(ang), sin(ang)} * prey_step, ang = (k-1) pi/4 (predator_prey.hpp:128-133)
+// predator_prey: prey_step = agility * max step size (predator_prey.hpp:68-72) and the
+// 8 compass offsets Vec2{cos(ang), sin(ang)} * prey_step, ang = (k-1) pi/4 (predator_prey.hpp:19-24)
 inline void prey_offsets(const mrsim_cfg& c, double* out16) {
     double robot_step = 0.0;
     for (int i = 0; i < c.num_robots; ++i) robot_step = robot_step < c.step_sizes[i] ? c.step_sizes[i] : robot_step;
@@ -353,11 +353,11 @@ template <int TASK, class Real>
 __device__ Real transition_task(const mrsim_cfg& c, EnvView<Real>& v, Rng& rng, Real& metric) {
     const int N = v.N;
     const mrsim_layout& L = c.layout;
-    if (TASK == MRSIM_TASK_NAVIGATION) {  // navigation.hpp:77-83
+    if (TASK == MRSIM_TASK_NAVIGATION) {  // navigation.hpp:45-51
         Real total = 0;
         for (int i = 0; i < N; ++i) total += dhypot(v.xs[i] - v.tf[2 * i], v.ys[i] - v.tf[2 * i + 1]);
         return Real(c.coef[MRSIM_COEF_DIST]) * total;
-    } else if (TASK == MRSIM_TASK_PREDATOR_PREY) {  // predator_prey.hpp:121-143, 183-199
+    } else if (TASK == MRSIM_TASK_PREDATOR_PREY) {  // predator_prey.hpp:15-34, 74-91
         Real bx, by;
         prey_heuristic_dev<Real>(c, v.prey_off, v.tf[0], v.tf[1], v.xs, v.ys, N, bx, by);
         v.tf[0] = bx;
@@ -371,7 +371,7 @@ __device__ Real transition_task(const mrsim_cfg& c, EnvView<Real>& v, Rng& rng, 
             v.ti[0] -= 1;
         }
         return tagged ? Real(c.coef[MRSIM_COEF_TAG]) : Real(0);
-    } else if (TASK == MRSIM_TASK_DISCOVERY) {  // discovery.hpp:256-283
+    } else if (TASK == MRSIM_TASK_DISCOVERY) {  // discovery.hpp:40-69
         const int K = L.discovery_num_landmarks;
         int sensed = v.ti[0], tagged = v.ti[1];
         int newly_sensed = 0, newly_tagged = 0;
@@ -442,7 +442,7 @@ __device__ Real transition_task(const mrsim_cfg& c, EnvView<Real>& v, Rng& rng, 
             }
         }
         return reward;
-    } else if (TASK == MRSIM_TASK_FORAGING) {  // foraging.hpp:214-231
+    } else if (TASK == MRSIM_TASK_FORAGING) {  // foraging.hpp:51-70
         const int M = L.foraging_num_resources;
         const Real radius = Real(L.foraging_radius);
         Real reward = 0;
@@ -550,7 +550,7 @@ __device__ Real transition_task(const mrsim_cfg& c, EnvView<Real>& v, Rng& rng, 
     }
 }
 
-// Scenario::finalize (navigation.hpp:85-93, arctic_transport.hpp:88-97).
+// Scenario::finalize (navigation.hpp:53-61, arctic_transport.hpp:88-97).
 template <int TASK, class Real>
 __device__ void finalize_task(const mrsim_cfg& c, const EnvView<Real>& v, Real& metric, int& success) {
     if (TASK == MRSIM_TASK_NAVIGATION) {
@@ -621,7 +621,7 @@ __device__ Real obs_feature(const mrsim_cfg& c, const EnvView<Real>& v, int r, i
             default: return Real(v.tf[2 * r + 1]);
         }
     }
-    if (TASK == MRSIM_TASK_NAVIGATION) {  // navigation.hpp:96-102
+    if (TASK == MRSIM_TASK_NAVIGATION) {  // navigation.hpp:64-70
         switch (q) {
             case 0: return Real(v.xs[r]);
             case 1: return Real(v.ys[r]);
@@ -641,7 +641,7 @@ __device__ Real obs_feature(const mrsim_cfg& c, const EnvView<Real>& v, int r, i
     }
     const int f = q - base;
     if (TASK == MRSIM_TASK_PREDATOR_PREY) return Real(v.tf[f]);
-    if (TASK == MRSIM_TASK_DISCOVERY) {  // discovery.hpp:287-298
+    if (TASK == MRSIM_TASK_DISCOVERY) {  // discovery.hpp:71-82
         const int k = f >> 1;
         const bool visible = ((v.ti[0] >> k) & 1) && !((v.ti[1] >> k) & 1);
         return Real(visible ? double(v.tf[f]) : L.discovery_sentinel[f & 1]);
@@ -657,7 +657,7 @@ __device__ Real obs_feature(const mrsim_cfg& c, const EnvView<Real>& v, int r, i
         if (g2 < rware_requests(L)) return Real(ti_byte(v.ti, S + N + g2));
         return Real(ti_byte(v.ti, S + r));
     }
-    if (TASK == MRSIM_TASK_FORAGING) {  // foraging.hpp:235-247
+    if (TASK == MRSIM_TASK_FORAGING) {  // foraging.hpp:72-84
         const int rr = f / 3, comp = f % 3;
         const bool live = !((v.ti[0] >> rr) & 1);
         if (comp < 2) return Real(live ? double(v.tf[2 * rr + comp]) : L.discovery_sentinel[comp]);
@@ -667,7 +667,7 @@ __device__ Real obs_feature(const mrsim_cfg& c, const EnvView<Real>& v, int r, i
         if (f == 0) return Real(v.tf[4 + r]);
         return Real(v.tf[f - 1]);  // 1 -> circle (tf[0]), 2 -> rect (tf[1])
     }
-    if (TASK == MRSIM_TASK_ARCTIC_TRANSPORT) {  // arctic_transport.hpp:199-220
+    if (TASK == MRSIM_TASK_ARCTIC_TRANSPORT) {  // arctic_transport.hpp:102-123
         if (f == 0) return Real(arctic_tile_at<Real>(c, v.ti, v.xs[r], v.ys[r]));
         const int g2 = f - 1;
         const int which = g2 / 9, cell = g2 % 9;
@@ -684,7 +684,7 @@ __device__ Real obs_feature(const mrsim_cfg& c, const EnvView<Real>& v, int r, i
         const bool in = rr >= 0 && rr < rows && cc >= 0 && cc < cols;
         return in ? Real(ti_byte(v.ti, rr * cols + cc)) : Real(0);
     }
-    // warehouse.hpp:284-290
+    // warehouse.hpp:57-63
     return ((v.ti[0] >> r) & 1) ? Real(1) : Real(0);
 }
 

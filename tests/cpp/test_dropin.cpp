@@ -127,7 +127,55 @@ static void compare_runs(const char* scenario, const char* policy, int episodes,
                 ref.rows.size(), flips, worst);
 }
 
+// Reference caller code written once against the reference's own signatures: the
+// function-pointer types below are exactly mrsim::reset_batch / mrsim::step_batch
+// (batch.hpp:240-290), and the device backend's functions bind to them unchanged.
+using ResetFn = std::pair<BatchWorldState, ResetOutput> (*)(const ScenarioConfig&, const std::vector<std::uint64_t>&,
+                                                            const Scenario&, WorkerPool*);
+using StepFn = std::pair<BatchWorldState, std::vector<StepOutput>> (*)(const BatchWorldState&, const std::vector<int>&,
+                                                                       const ScenarioConfig&, const Scenario&,
+                                                                       WorkerPool*);
+
+static BatchWorldState caller(ResetFn reset, StepFn step, const ScenarioConfig& cfg,
+                              const std::vector<std::uint64_t>& seeds, int T, WorkerPool* pool,
+                              std::vector<double>& rewards) {
+    const ScenarioPtr scenario = make_scenario(cfg.scenario_name);
+    auto [state, obs] = reset(cfg, seeds, *scenario, pool);
+    for (int t = 0; t < T; ++t) {
+        std::vector<int> actions;
+        for (std::size_t e = 0; e < seeds.size(); ++e)
+            for (int r = 0; r < cfg.num_robots; ++r)
+                actions.push_back(static_cast<int>(policy_stream(seeds[e], t, r).uniform_int(kNumActions)));
+        auto [next, outs] = step(state, actions, cfg, *scenario, pool);
+        for (const auto& o : outs) rewards.push_back(o.team_reward);
+        state = std::move(next);
+    }
+    return state;
+}
+
+static void compare_reference_signature() {
+    const ScenarioConfig cfg = config_for("navigation", 4);
+    std::vector<std::uint64_t> seeds;
+    for (int e = 0; e < 3000; ++e) seeds.push_back(derive_episode_seed(8, e));
+    WorkerPool pool(4);
+    std::vector<double> ra, da;
+    const BatchWorldState rs = caller(&mrsim::reset_batch, &mrsim::step_batch, cfg, seeds, 30, &pool, ra);
+    const BatchWorldState ds = caller(&mrsim::cuda::reset_batch, &mrsim::cuda::step_batch, cfg, seeds, 30, &pool, da);
+    double worst = 0, rworst = 0;
+    for (std::size_t e = 0; e < seeds.size(); ++e) {
+        EXPECT(rs.envs[e].step_index == ds.envs[e].step_index, "signature path step_index e%zu", e);
+        EXPECT(rs.envs[e].metrics.collisions == ds.envs[e].metrics.collisions, "signature path collisions");
+        for (int i = 0; i < 4; ++i)
+            worst = std::fmax(worst, std::fabs(rs.envs[e].poses[i].x - ds.envs[e].poses[i].x));
+    }
+    for (std::size_t k = 0; k < ra.size(); ++k) rworst = std::fmax(rworst, std::fabs(ra[k] - da[k]));
+    EXPECT(worst <= 1e-9 && rworst <= 1e-9, "signature path pose %.3g reward %.3g", worst, rworst);
+    std::printf("reference-signature step_batch (cached engine, WorkerPool(4)): B=3000 x 30 steps, max pose diff "
+                "%.3g, max reward diff %.3g\n", worst, rworst);
+}
+
 int main() {
+    compare_reference_signature();
     compare_runs("navigation", "random", 6, 4, 30);
     compare_runs("warehouse", "scripted_goal", 3, 3, 20);
     compare_runs("predator_prey", "prey_chaser", 3, 2, 20);

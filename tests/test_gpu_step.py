@@ -103,7 +103,7 @@ def test_reset_matches_reference(task, n, fp64, ref):
         assert sa.rng_key == sb.rng_key
 
 
-def _teacher_forced(ref, task, n, fp64, sub_steps, T, B=48, max_steps=0, controller=-1):
+def _teacher_forced(ref, task, n, fp64, sub_steps, T, B=48, max_steps=0, controller=-1, **batch_kw):
     cfg, sp = make_cfgs(ref, task, n, max_steps=max_steps, controller=controller)
     if sub_steps:
         cfg.sub_steps = sub_steps
@@ -111,7 +111,7 @@ def _teacher_forced(ref, task, n, fp64, sub_steps, T, B=48, max_steps=0, control
     seeds = [m.derive_episode_seed(1, e) for e in range(B)]
     rb = ref.RefBatch(sp)
     rb.reset(seeds)
-    gb = m.CudaEnvBatch(cfg, B, fp64=fp64)
+    gb = m.CudaEnvBatch(cfg, B, fp64=fp64, **batch_kw)
     stats = {"pose": 0.0, "angle": 0.0, "real": 0.0, "discrete": [], "reward_bad": 0, "obs": 0.0}
     for t in range(T):
         st = rb.get_states()
@@ -405,3 +405,70 @@ def test_fp32_fast_mode_new_paths_track_reference(task, n, controller, ref):
     cfg, st = _teacher_forced(ref, task, n, False, 1, 40, max_steps=60, controller=controller)
     assert st["pose"] <= 2e-6 and st["angle"] <= 4e-5, st
     assert len(st["discrete"]) <= 1, st["discrete"][:5]
+
+
+@pytest.mark.parametrize("env_per_thread", [False, True])
+def test_rollback_after_more_than_64_queued_steps(env_per_thread):
+    """A failing device step followed by 70 queued (no-op) steps before the sync: the state is
+    rolled back to the failing step's input (step_batch is pure, batch.hpp:267-290)."""
+    import torch
+    cfg = m.make_default_config("navigation")
+    gb = m.CudaEnvBatch(cfg, 64, env_per_thread=env_per_thread)
+    gb.reset_seeds(list(range(64)))
+    good = torch.zeros((64, 3), dtype=torch.int8, device="cuda")
+    gb.step(good)
+    gb.sync()
+    before = gb.get_states()
+    bad = good.clone()
+    bad[17, 2] = 5
+    gb.step(bad)
+    for _ in range(70):
+        gb.step(good)
+    with pytest.raises(m.InvalidArgument, match=r"environment 17, robot 2"):
+        gb.sync()
+    after = gb.get_states()
+    assert [list(s.x[:3]) for s in before] == [list(s.x[:3]) for s in after]
+    assert [s.step_index for s in before] == [s.step_index for s in after]
+    gb.step(good)  # the context stays usable
+    gb.sync()
+    assert gb.get_states(0, 1)[0].step_index == before[0].step_index + 1
+
+
+@pytest.mark.parametrize("env_per_thread", [False, True])
+def test_failed_step_rolls_back_episode_stats(env_per_thread):
+    """Every env finishes its episode on the failing step; the envs that completed before the
+    error was noticed must not keep their EpisodeStats update (no double count on retry)."""
+    cfg = m.make_default_config("navigation")
+    B = 200
+    gb = m.CudaEnvBatch(cfg, B, env_per_thread=env_per_thread)
+    gb.reset_seeds([m.derive_episode_seed(0, e) for e in range(B)])
+    st = list(gb.get_states())
+    for s in st:
+        s.step_index = cfg.raw.max_steps - 1
+    gb.set_states(st)
+    acts = np.zeros((B, 3), dtype=np.int32)
+    acts[150, 0] = 9
+    with pytest.raises(m.InvalidArgument):
+        gb.step_host(acts)
+    assert gb.stats()["episodes"] == 0
+    acts[150, 0] = 0
+    gb.step_host(acts)
+    assert gb.stats()["episodes"] == B
+
+
+@pytest.mark.parametrize("env_per_thread", [False, True])
+def test_invalid_action_outranks_a_physics_error_in_a_lower_env(env_per_thread):
+    """validate_actions runs over every env before any env steps (batch.hpp:271): an invalid
+    action in env 5 is reported even though env 3 has coincident robots (domain_error)."""
+    cfg = m.make_default_config("navigation")
+    gb = m.CudaEnvBatch(cfg, 8, env_per_thread=env_per_thread)
+    gb.reset_seeds(list(range(8)))
+    st = list(gb.get_states())
+    st[3].x[1], st[3].y[1], st[3].theta[1] = st[3].x[0], st[3].y[0], st[3].theta[0]
+    gb.set_states(st)
+    acts = np.zeros((8, 3), dtype=np.int32)
+    with pytest.raises(m.DomainError, match=r"environment 3"):
+        gb.step_host(acts)
+    acts[5, 1] = 7
+    with pytest.raises(m.InvalidArgument, match=r"invalid action 7 for environment 5, robot 1"):
+        gb.step_host(acts)
