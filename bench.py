@@ -227,26 +227,72 @@ def roofline(a, cfg, per_gpu: float, kernel_ms: float, fp64: bool, pipe_peak_tfl
 
 
 class ClockSampler:
-    def __init__(self, gpu: int):
-        self.path = f"/tmp/mrsim_clocks_{os.getpid()}.csv"
-        self.proc = None
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(gpu), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
-                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-        except Exception:
-            self.proc = None
+    """SM clock and throttle reasons sampled DURING the timed region: NVML polled from a thread
+    every ~1 ms (the timed region of a short run lasts a few ms), nvidia-smi as the fallback."""
+    REASONS = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
-    def stop(self):
+    def __init__(self, gpu: int):
+        import threading
+
+        self.samples, self.mx, self.reasons = [], 0.0, set()
+        self.stop_ev = threading.Event()
+        self.proc = None
+        self.thread = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(gpu)
+            bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+            self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+
+            def poll():
+                while not self.stop_ev.is_set():
+                    self.samples.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.reasons.update(k for k, v in bits.items() if r & v)
+                    time.sleep(0.001)
+            self.thread = threading.Thread(target=poll, daemon=True)
+            self.thread.start()
+            self.source = "nvml"
+        except Exception:
+            self.source = "nvidia-smi"
+            self.path = f"/tmp/mrsim_clocks_{os.getpid()}.csv"
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(gpu), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                     "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                     "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                     "--format=csv,noheader,nounits", "-lms", "50"],
+                    stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            except Exception:
+                self.proc = None
+
+    def wait_first(self, timeout: float = 2.0) -> None:
+        t0 = time.time()
+        while self.thread is not None and not self.samples and time.time() - t0 < timeout:
+            time.sleep(0.0005)
+
+    def mark(self) -> int:
+        return len(self.samples)
+
+    def stop(self, since: int = 0):
+        if self.thread is not None:
+            self.stop_ev.set()
+            self.thread.join()
+            sm = self.samples[since:] or self.samples[-1:]
+            if not sm:
+                return None
+            return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": self.mx, "reasons": sorted(self.reasons),
+                    "samples": len(sm), "source": "nvml, 1 ms polling during the timed region"}
         if not self.proc:
             return None
         self.proc.terminate()
         self.proc.wait()
         sm, mx, reasons = [], 0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in open(self.path):
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 7:
@@ -256,12 +302,17 @@ class ClockSampler:
                 mx = max(mx, float(parts[1]))
             except ValueError:
                 continue
-            for nm, v in zip(names, parts[3:7]):
+            for nm, v in zip(self.REASONS, parts[3:7]):
                 if v.lower() == "active":
                     reasons.add(nm)
         if not sm:
             return None
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvidia-smi -lms 50"}
+
+
+def finite(v):
+    return v if v is None or np.isfinite(v) else None
 
 
 def dump_states(path: str, rank: int, shard, batch) -> None:
@@ -322,9 +373,12 @@ def main():
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
     clocks = ClockSampler(local) if rank == 0 else None
+    if clocks:
+        clocks.wait_first()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
+    mark = clocks.mark() if clocks else 0
     w0 = time.perf_counter()
     for k in range(a.steps):
         if not a.no_flush:
@@ -337,7 +391,7 @@ def main():
     if dist:
         dist.barrier()
     batch.sync()
-    clk = clocks.stop() if clocks else None
+    clk = clocks.stop(mark) if clocks else None
     dev_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
     t_local = torch.tensor([dev_ms], dtype=torch.float64, device=rdev)
     if dist:
@@ -425,7 +479,7 @@ def main():
             "episodes": {"completed": stats["episodes"], "mean_return": stats["mean_return"],
                          "collisions": stats["sum_collisions"], "success": stats["sum_success"],
                          "qp_infeasible": stats["sum_qp_infeasible"],
-                         "min_pairwise_distance": stats["min_pairwise_distance"]},
+                         "min_pairwise_distance": finite(stats["min_pairwise_distance"])},
         }
         if verify is not None:
             line["verify"] = verify

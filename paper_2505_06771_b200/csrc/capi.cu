@@ -7,7 +7,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "launch.h"
@@ -52,6 +54,7 @@ struct mrsim_ctx {
     double* d_reward64 = nullptr;
     uint8_t* d_done = nullptr;
     unsigned long long* h_err = nullptr;  // pinned copy of the device error word + serial
+    void* h_state = nullptr;              // pinned host mirror of one state copy (state I/O)
     int32_t* d_actions32 = nullptr;
     bool reset_done = false;
     // on-device policy: feedforward network (mrsim_set_policy_feedforward) or scripted (kind != 0)
@@ -449,40 +452,93 @@ int do_reset(mrsim_ctx* ctx, DevState<Real>* s, const uint64_t* d_seeds, uint64_
     return MRSIM_OK;
 }
 
+// fn(k) for k in [0, count) on the host's cores (state conversions of large batches).
+template <class F>
+void host_parallel_for(long long count, F&& fn) {
+    const long long T = static_cast<long long>(std::thread::hardware_concurrency());
+    if (count < 8192 || T <= 1) {
+        for (long long k = 0; k < count; ++k) fn(k);
+        return;
+    }
+    const long long per = (count + T - 1) / T;
+    std::vector<std::thread> pool;
+    for (long long t = 0; t < T; ++t)
+        pool.emplace_back([&, t] {
+            const long long lo = t * per, hi = std::min(count, lo + per);
+            for (long long k = lo; k < hi; ++k) fn(k);
+        });
+    for (auto& th : pool) th.join();
+}
+
+// Pinned host mirror of one state copy, carved exactly like the device copies.
+template <class Real>
+cudaError_t host_mirror(mrsim_ctx* ctx, DevState<Real>& h) {
+    if (!ctx->h_state) {
+        const cudaError_t e = cudaMallocHost(&ctx->h_state, state_bytes<Real>(ctx->B, ctx->N, ctx->nf, ctx->ni));
+        if (e != cudaSuccess) {
+            ctx->h_state = nullptr;
+            return e;
+        }
+    }
+    carve_state(ctx->h_state, ctx->B, ctx->N, ctx->nf, ctx->ni, h);
+    return cudaSuccess;
+}
+
+// Copy envs [first, first + count) of every field between a device state copy and the host
+// mirror: the whole block in one transfer for the full batch, else one slice per field.
+template <class Real>
+cudaError_t copy_state_slices(mrsim_ctx* ctx, const DevState<Real>& d, const DevState<Real>& h, long long first,
+                              long long count, cudaMemcpyKind kind) {
+    const bool up = kind == cudaMemcpyHostToDevice;
+    if (first == 0 && count == ctx->B) {
+        const size_t sb = state_bytes<Real>(ctx->B, ctx->N, ctx->nf, ctx->ni);
+        return up ? cudaMemcpy(d.px, h.px, sb, kind) : cudaMemcpy(h.px, d.px, sb, kind);
+    }
+    cudaError_t e = cudaSuccess;
+    auto cp = [&](void* dv, void* hv, size_t bytes) {
+        if (e == cudaSuccess) e = up ? cudaMemcpy(dv, hv, bytes, kind) : cudaMemcpy(hv, dv, bytes, kind);
+    };
+    const int N = ctx->N;
+    cp(d.px + first * N, h.px + first * N, sizeof(Real) * count * N);
+    cp(d.py + first * N, h.py + first * N, sizeof(Real) * count * N);
+    cp(d.pt + first * N, h.pt + first * N, sizeof(Real) * count * N);
+    cp(d.step_index + first, h.step_index + first, 4 * count);
+    cp(d.key + first, h.key + first, 8 * count);
+    cp(d.seed + first, h.seed + first, 8 * count);
+    cp(d.pkey + first, h.pkey + first, 8 * count);
+    cp(d.episode + first, h.episode + first, 8 * count);
+    cp(d.collisions + first, h.collisions + first, 4 * count);
+    cp(d.qp_inf + first, h.qp_inf + first, 4 * count);
+    cp(d.success + first, h.success + first, 4 * count);
+    cp(d.metric + first, h.metric + first, sizeof(Real) * count);
+    cp(d.min_dist + first, h.min_dist + first, sizeof(Real) * count);
+    cp(d.ep_return + first, h.ep_return + first, sizeof(Real) * count);
+    for (int f = 0; f < ctx->nf; ++f) cp(d.tf + f * ctx->B + first, h.tf + f * ctx->B + first, sizeof(Real) * count);
+    for (int w = 0; w < ctx->ni; ++w) cp(d.ti + w * ctx->B + first, h.ti + w * ctx->B + first, 4 * count);
+    return e;
+}
+
 template <class Real>
 void to_host_states(mrsim_ctx* ctx, const DevState<Real>& s, long long first, long long count,
                     mrsim_env_state* out, cudaError_t* err) {
     const int N = ctx->N;
-    std::vector<Real> px(count * N), py(count * N), pt(count * N), metric(count), mind(count), ret(count);
-    std::vector<int32_t> step(count), coll(count), qpi(count), succ(count);
-    std::vector<uint64_t> key(count), seed(count);
-    std::vector<int64_t> ep(count);
-    std::vector<Real> tf(static_cast<size_t>(count) * (ctx->nf > 0 ? ctx->nf : 1));
-    std::vector<int32_t> ti(static_cast<size_t>(count) * (ctx->ni > 0 ? ctx->ni : 1));
-    cudaError_t e = cudaSuccess;
-    auto cp = [&](void* dst, const void* src, size_t bytes) {
-        if (e == cudaSuccess) e = cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost);
-    };
-    cp(px.data(), s.px + first * N, sizeof(Real) * count * N);
-    cp(py.data(), s.py + first * N, sizeof(Real) * count * N);
-    cp(pt.data(), s.pt + first * N, sizeof(Real) * count * N);
-    cp(step.data(), s.step_index + first, 4 * count);
-    cp(key.data(), s.key + first, 8 * count);
-    cp(seed.data(), s.seed + first, 8 * count);
-    cp(ep.data(), s.episode + first, 8 * count);
-    cp(coll.data(), s.collisions + first, 4 * count);
-    cp(qpi.data(), s.qp_inf + first, 4 * count);
-    cp(succ.data(), s.success + first, 4 * count);
-    cp(metric.data(), s.metric + first, sizeof(Real) * count);
-    cp(mind.data(), s.min_dist + first, sizeof(Real) * count);
-    cp(ret.data(), s.ep_return + first, sizeof(Real) * count);
-    for (int f = 0; f < ctx->nf; ++f) cp(tf.data() + f * count, s.tf + f * ctx->B + first, sizeof(Real) * count);
-    for (int w = 0; w < ctx->ni; ++w) cp(ti.data() + w * count, s.ti + w * ctx->B + first, 4 * count);
+    // the device SoA block (or the requested env slice of each field) into its pinned host mirror
+    DevState<Real> h;
+    cudaError_t e = host_mirror<Real>(ctx, h);
+    if (e == cudaSuccess) e = copy_state_slices<Real>(ctx, s, h, first, count, cudaMemcpyDeviceToHost);
+    const Real *px = h.px + first * N, *py = h.py + first * N, *pt = h.pt + first * N;
+    const Real *metric = h.metric + first, *mind = h.min_dist + first, *ret = h.ep_return + first;
+    const int32_t *step = h.step_index + first, *coll = h.collisions + first, *qpi = h.qp_inf + first,
+                  *succ = h.success + first;
+    const uint64_t *key = h.key + first, *seed = h.seed + first;
+    const int64_t* ep = h.episode + first;
+    const Real* tf = h.tf + first;
+    const int32_t* ti = h.ti + first;
     *err = e;
     if (e != cudaSuccess) return;
     const mrsim_cfg& c = ctx->cfg;
     const mrsim_layout& y = c.layout;
-    for (long long k = 0; k < count; ++k) {
+    host_parallel_for(count, [&](long long k) {
         mrsim_env_state& o = out[k];
         std::memset(&o, 0, sizeof o);
         o.num_robots = N;
@@ -501,8 +557,8 @@ void to_host_states(mrsim_ctx* ctx, const DevState<Real>& s, long long first, lo
         o.scenario_metric = double(metric[k]);
         o.min_pairwise_distance = double(mind[k]);
         o.episode_return = double(ret[k]);
-        auto TF = [&](int f) { return double(tf[static_cast<size_t>(f) * count + k]); };
-        auto TI = [&](int w) { return ti[static_cast<size_t>(w) * count + k]; };
+        auto TF = [&](int f) { return double(tf[static_cast<size_t>(f) * ctx->B + k]); };
+        auto TI = [&](int w) { return ti[static_cast<size_t>(w) * ctx->B + k]; };
         auto TB = [&](int b) { return (TI(b >> 2) >> (8 * (b & 3))) & 0xff; };
         switch (c.task) {
             case MRSIM_TASK_NAVIGATION:
@@ -559,7 +615,7 @@ void to_host_states(mrsim_ctx* ctx, const DevState<Real>& s, long long first, lo
                 }
                 break;
         }
-    }
+    });
 }
 
 template <class Real>
@@ -568,13 +624,23 @@ void from_host_states(mrsim_ctx* ctx, const DevState<Real>& s, long long first, 
     const int N = ctx->N;
     const mrsim_cfg& c = ctx->cfg;
     const mrsim_layout& y = c.layout;
-    std::vector<Real> px(count * N), py(count * N), pt(count * N), metric(count), mind(count), ret(count);
-    std::vector<int32_t> step(count), coll(count), qpi(count), succ(count);
-    std::vector<uint64_t> key(count), seed(count), pkey(count);
-    std::vector<int64_t> ep(count);
-    std::vector<Real> tf(static_cast<size_t>(count) * (ctx->nf > 0 ? ctx->nf : 1), Real(0));
-    std::vector<int32_t> ti(static_cast<size_t>(count) * (ctx->ni > 0 ? ctx->ni : 1), 0);
-    for (long long k = 0; k < count; ++k) {
+    DevState<Real> h;
+    cudaError_t e = host_mirror<Real>(ctx, h);
+    if (e != cudaSuccess) {
+        *err = e;
+        return;
+    }
+    Real *px = h.px + first * N, *py = h.py + first * N, *pt = h.pt + first * N;
+    Real *metric = h.metric + first, *mind = h.min_dist + first, *ret = h.ep_return + first;
+    int32_t *step = h.step_index + first, *coll = h.collisions + first, *qpi = h.qp_inf + first,
+            *succ = h.success + first;
+    uint64_t *key = h.key + first, *seed = h.seed + first, *pkey = h.pkey + first;
+    int64_t* ep = h.episode + first;
+    Real* tf = h.tf + first;
+    int32_t* ti = h.ti + first;
+    host_parallel_for(count, [&](long long k) {
+        for (int f = 0; f < ctx->nf; ++f) tf[static_cast<size_t>(f) * ctx->B + k] = Real(0);
+        for (int w = 0; w < ctx->ni; ++w) ti[static_cast<size_t>(w) * ctx->B + k] = 0;
         const mrsim_env_state& o = in[k];
         for (int i = 0; i < N; ++i) {
             px[k * N + i] = Real(o.x[i]);
@@ -592,10 +658,10 @@ void from_host_states(mrsim_ctx* ctx, const DevState<Real>& s, long long first, 
         metric[k] = Real(o.scenario_metric);
         mind[k] = Real(o.min_pairwise_distance);
         ret[k] = Real(o.episode_return);
-        auto TF = [&](int f, double v) { tf[static_cast<size_t>(f) * count + k] = Real(v); };
-        auto TI = [&](int w, int v) { ti[static_cast<size_t>(w) * count + k] = v; };
+        auto TF = [&](int f, double v) { tf[static_cast<size_t>(f) * ctx->B + k] = Real(v); };
+        auto TI = [&](int w, int v) { ti[static_cast<size_t>(w) * ctx->B + k] = v; };
         auto TB = [&](int b, int v) {
-            int32_t& w = ti[static_cast<size_t>(b >> 2) * count + k];
+            int32_t& w = ti[static_cast<size_t>(b >> 2) * ctx->B + k];
             const int sh = 8 * (b & 3);
             w = (w & ~(0xff << sh)) | ((v & 0xff) << sh);
         };
@@ -657,27 +723,8 @@ void from_host_states(mrsim_ctx* ctx, const DevState<Real>& s, long long first, 
                 }
                 break;
         }
-    }
-    cudaError_t e = cudaSuccess;
-    auto cp = [&](void* dst, const void* src, size_t bytes) {
-        if (e == cudaSuccess) e = cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice);
-    };
-    cp(s.px + first * N, px.data(), sizeof(Real) * count * N);
-    cp(s.py + first * N, py.data(), sizeof(Real) * count * N);
-    cp(s.pt + first * N, pt.data(), sizeof(Real) * count * N);
-    cp(s.step_index + first, step.data(), 4 * count);
-    cp(s.key + first, key.data(), 8 * count);
-    cp(s.seed + first, seed.data(), 8 * count);
-    cp(s.pkey + first, pkey.data(), 8 * count);
-    cp(s.episode + first, ep.data(), 8 * count);
-    cp(s.collisions + first, coll.data(), 4 * count);
-    cp(s.qp_inf + first, qpi.data(), 4 * count);
-    cp(s.success + first, succ.data(), 4 * count);
-    cp(s.metric + first, metric.data(), sizeof(Real) * count);
-    cp(s.min_dist + first, mind.data(), sizeof(Real) * count);
-    cp(s.ep_return + first, ret.data(), sizeof(Real) * count);
-    for (int f = 0; f < ctx->nf; ++f) cp(s.tf + f * ctx->B + first, tf.data() + f * count, sizeof(Real) * count);
-    for (int w = 0; w < ctx->ni; ++w) cp(s.ti + w * ctx->B + first, ti.data() + w * count, 4 * count);
+    });
+    e = copy_state_slices<Real>(ctx, s, h, first, count, cudaMemcpyHostToDevice);
     *err = e;
 }
 
@@ -883,6 +930,7 @@ void mrsim_destroy(mrsim_ctx* ctx) {
     cudaFree(ctx->d_reward64);
     cudaFree(ctx->d_done);
     if (ctx->h_err) cudaFreeHost(ctx->h_err);
+    if (ctx->h_state) cudaFreeHost(ctx->h_state);
     cudaFree(ctx->d_wT);
     cudaFree(ctx->d_bias);
     cudaFree(ctx->d_pol_actions);

@@ -381,29 +381,6 @@ __device__ __forceinline__ int env_qp_solve(const EnvRows<Real>& rows, Real (&ux
     return status;
 }
 
-template <class Real>
-struct Real2 {
-    Real a, b;
-};
-
-// unicycle_pose_controller (controllers.hpp:68-82): out of line, so the position
-// controller's tick loop (the benchmark path) stays small in the instruction cache.
-template <class Real>
-__device__ __noinline__ Real2<Real> pose_nominal(const PhysConsts<Real>& K, Real x, Real y, Real th, Real wpx,
-                                                 Real wpy, Real wh) {
-    Real2<Real> out{Real(0), Real(0)};
-    const Real dx = wpx - x, dy = wpy - y;
-    const Real rho = dhypot(dx, dy);
-    const Real herr = wrap_angle_dev(wh - th);
-    if (!(rho < K.pose_ptol && dabs(herr) < K.pose_htol)) {
-        const Real alpha = wrap_angle_dev(atan2(dy, dx) - th);
-        const Real beta = wrap_angle_dev(wh - th - alpha);
-        out.a = dclamp(K.k_rho * rho, -K.v_max, K.v_max);
-        out.b = dclamp(K.k_alpha * alpha + K.k_beta * beta, -K.w_max, K.w_max);
-    }
-    return out;
-}
-
 // The QP iterate in and out of env_qp (by value: the rare QP path is an out-of-line
 // call, so the common tick -- nothing violated at u_nom -- keeps its registers).
 template <class Real>

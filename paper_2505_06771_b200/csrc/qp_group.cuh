@@ -65,16 +65,18 @@ struct QpWs {
 // empty active set (same arithmetic; a speed/register-pressure trade chosen
 // per task, see qp_fast_first_row in step_kernel.cuh).
 //
-// Warm entering order (warm_k != nullptr): the rows active at the end of the
-// group's previous solve (ws.warm, *warm_k of them, rebuilt on this tick's
-// geometry) are offered as the entering rows of the first iterations, in
-// their previous order, instead of the most violated row of a scan; a row no
-// longer violated is passed over (the inner loop leaves u unchanged). The
-// iteration is otherwise the method above, so it reaches the same unique
-// optimum (strictly convex QP): only the internal path, and so rounding at
-// the 1e-16 level, differs from the cold most-violated-first order. A warp
-// skips its row scan while every group still has a warm row to offer.
-template <class Real, int L, bool FAST = true, class RowSet>
+// Warm start (WARM, warm_k != nullptr; Goldfarb-Idnani from a dual-feasible
+// point): the rows active at the end of the group's previous solve (ws.warm,
+// *warm_k of them, in their logical order) are re-entered on this tick's
+// geometry by bordered-inverse updates alone (no scans, no steps), the
+// multipliers of that set are solved directly, lam = S (N^T u_nom - h), and
+// u = u_nom - N lam. If every multiplier is >= 0 this is a valid state of the
+// dual method (dual feasible, the active rows tight), and the ordinary
+// iteration continues from it: it adds whatever rows are still violated
+// (usually none) and stops at the same unique optimum of the strictly convex
+// QP as the cold start. A negative multiplier (the set changed) or a
+// dependent row falls back to the cold start from u_nom.
+template <class Real, int L, bool FAST = true, bool WARM = false, class RowSet>
 __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpWs<Real, typename RowSet::Desc>& ws,
                                         int n, bool participate, Real& ux, Real& uy, int total_rows, Real tol,
                                         int* warm_k = nullptr) {
@@ -91,22 +93,144 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
     bool done = !participate;
     int iter = 0;
     const int max_iterations = 100 + 20 * total_rows;  // qp.hpp:193
-    const int wk = (warm_k && participate) ? *warm_k : 0;  // warm rows on offer (group-uniform)
-    int wi = 0;
+    if constexpr (WARM) {
+        const int wk = participate ? *warm_k : 0;  // previous active rows (group-uniform)
+        const int wmax = Grp<L>::warp_max(wk);
+        if (wmax > 0) {
+            const Real ux0 = ux, uy0 = uy;
+            bool wok = wk > 0;
+            // 1) S for the previous active set, one bordered-inverse update per row, in logical order
+            for (int j = 0; j < wmax; ++j) {
+                const bool act = wok && j < wk;
+                const Desc gd = rows.describe(g, act ? ws.warm[j] : rows.dummy_row());
+                Real gx, gy;
+                rows.comp(gd, lane, gx, gy);
+                if (!vl) gx = Real(0);
+                if (!vly) gy = Real(0);
+                const bool s0 = act && lp0 >= 0, s1 = act && lp1 >= 0;
+                if (s0) ws.d[q0] = rows.dot(ws.desc[q0], gd);
+                if (s1) ws.d[q1] = rows.dot(ws.desc[q1], gd);
+                Grp<L>::sync();
+                Real r0 = 0, r1 = 0;
+                if (s0) {
+                    for (unsigned m = amask; m; m &= m - 1) {
+                        const int c = __ffs(m) - 1;
+                        r0 += ws.S[q0 * n + c] * ws.d[c];
+                    }
+                    ws.r[q0] = r0;
+                }
+                if (s1) {
+                    for (unsigned m = amask; m; m &= m - 1) {
+                        const int c = __ffs(m) - 1;
+                        r1 += ws.S[q1 * n + c] * ws.d[c];
+                    }
+                    ws.r[q1] = r1;
+                }
+                Grp<L>::sync();
+                Real zx = gx, zy = gy;
+                if (act && vl) {
+                    for (unsigned m = tm; m; m &= m - 1) {
+                        const int c = __ffs(m) - 1;
+                        Real cx, cy;
+                        rows.comp(ws.desc[c], lane, cx, cy);
+                        zx -= ws.r[c] * cx;
+                        zy -= ws.r[c] * cy;
+                    }
+                }
+                if (!vly) zy = Real(0);
+                const Real z2 = g.sum(zx * zx + zy * zy);
+                if (act && !(z2 > Prec<Real>::eps_z)) wok = false;  // dependent now: cold start
+                if (act && wok) {  // bordered inverse (as in the inner loop's add)
+                    const Real is = Real(1) / z2;
+                    const int qk = __ffs(~amask) - 1;
+                    if (s0) {
+                        const Real ra = r0 * is;
+                        for (unsigned m = amask; m; m &= m - 1) {
+                            const int c = __ffs(m) - 1;
+                            ws.S[q0 * n + c] += ra * ws.r[c];
+                        }
+                        ws.S[q0 * n + qk] = -ra;
+                        ws.S[qk * n + q0] = -ra;
+                    }
+                    if (s1) {
+                        const Real ra = r1 * is;
+                        for (unsigned m = amask; m; m &= m - 1) {
+                            const int c = __ffs(m) - 1;
+                            ws.S[q1 * n + c] += ra * ws.r[c];
+                        }
+                        ws.S[q1 * n + qk] = -ra;
+                        ws.S[qk * n + q1] = -ra;
+                    }
+                    if (lane == (qk & (L - 1))) {
+                        ws.S[qk * n + qk] = is;
+                        ws.act[qk] = ws.warm[j];
+                        ws.desc[qk] = gd;
+                        if (qk < L) lp0 = k;
+                        else lp1 = k;
+                    }
+                    if (rows.touches(gd, lane)) tm |= 1u << qk;
+                    amask |= 1u << qk;
+                    rows.set_active(g, ws.warm[j], true);
+                    ++k;
+                }
+                Grp<L>::sync();
+            }
+            // 2) lam = S (N^T u_nom - h), u = u_nom - N lam
+            rows.publish_u(lane, ux0, uy0);
+            Grp<L>::sync();
+            const bool w0 = wok && lp0 >= 0, w1 = wok && lp1 >= 0;
+            if (w0) ws.d[q0] = rows.dot_u(ws.desc[q0]) - rows.rhs(ws.desc[q0]);
+            if (w1) ws.d[q1] = rows.dot_u(ws.desc[q1]) - rows.rhs(ws.desc[q1]);
+            Grp<L>::sync();
+            Real l0 = 0, l1 = 0;
+            if (w0) {
+                for (unsigned m = amask; m; m &= m - 1) {
+                    const int c = __ffs(m) - 1;
+                    l0 += ws.S[q0 * n + c] * ws.d[c];
+                }
+                ws.lam[q0] = l0;
+            }
+            if (w1) {
+                for (unsigned m = amask; m; m &= m - 1) {
+                    const int c = __ffs(m) - 1;
+                    l1 += ws.S[q1 * n + c] * ws.d[c];
+                }
+                ws.lam[q1] = l1;
+            }
+            // 3) dual feasibility of the warm point, else the cold start
+            if (g.any((w0 && l0 < Real(0)) || (w1 && l1 < Real(0)))) wok = false;
+            Grp<L>::sync();
+            if (wok) {
+                for (unsigned m = tm; m; m &= m - 1) {
+                    const int c = __ffs(m) - 1;
+                    Real cx, cy;
+                    rows.comp(ws.desc[c], lane, cx, cy);
+                    ux -= ws.lam[c] * cx;
+                    uy -= ws.lam[c] * cy;
+                }
+                if (!vl) ux = Real(0);
+                if (!vly) uy = Real(0);
+            } else {  // cold start: empty active set at u_nom
+                ux = ux0;
+                uy = uy0;
+                lp0 = lp1 = -1;
+                amask = tm = 0u;
+                k = 0;
+                rows.active = 0u;
+            }
+            Grp<L>::sync();
+        }
+    }
     while (Grp<L>::warp_any(!done)) {
         if (!done && iter >= max_iterations) {
             status = kQpIterLimit;
             done = true;
         }
-        // Most violated inactive row (qp.hpp:225-239), or the next warm row.
+        // Most violated inactive row (qp.hpp:225-239).
         Real worst = tol;
         int p = -1;
-        const bool forced = !done && wi < wk;
-        if (Grp<L>::warp_any(!done && !forced)) {
-            rows.scan(g, ux, uy, worst, p);
-            g.argmax(worst, p);
-        }
-        if (forced) p = ws.warm[wi++];
+        rows.scan(g, ux, uy, worst, p);
+        g.argmax(worst, p);
         if (!done && p < 0) done = true;
         if (!Grp<L>::warp_any(!done)) break;  // every env of the warp is optimal
         bool act = !done;
@@ -324,10 +448,10 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
             if (in && guard > total_rows) in = false;  // guard exhausted without adding
             Grp<L>::sync();
         }
-        if (act && !added && !forced) done = true;  // stall (qp.hpp:331-334) or infeasible
+        if (act && !added) done = true;  // stall (qp.hpp:331-334) or infeasible
         if (act) ++iter;
     }
-    if (warm_k) {  // remember this solve's active rows, in logical order
+    if constexpr (WARM) {  // remember this solve's active rows, in logical order
         if (participate && lp0 >= 0) ws.warm[lp0] = ws.act[q0];
         if (participate && lp1 >= 0) ws.warm[lp1] = ws.act[q1];
         *warm_k = (participate && status == kQpOptimal) ? k : 0;

@@ -308,6 +308,18 @@ struct BarrierRows {
         return s;
     }
 
+    // u of every robot of the group published in the row cache (the scan's slots), and a row's u
+    __device__ __forceinline__ void publish_u(int lane, Real ux, Real uy) const {
+        F(kU, lane) = ux;
+        F(kU + 1, lane) = uy;
+    }
+    __device__ __forceinline__ Real dot_u(const Desc& d) const {
+        const Real s0 = (d.r1 >= 0) ? Real(-1) : Real(1);
+        Real v = s0 * (d.cx * F(kU, d.r0) + d.cy * F(kU + 1, d.r0));
+        if (d.r1 >= 0) v += d.cx * F(kU, d.r1) + d.cy * F(kU + 1, d.r1);
+        return v;
+    }
+
     __device__ __forceinline__ void set_active(const Grp<L>& g, int p, bool on) {
         int owner, bit;
         if (p < P) {
@@ -366,7 +378,7 @@ __device__ __forceinline__ void init_rows(BarrierRows<Real, L, MP, MO>& rows, Re
 // QP, infeasible -> zero commands, else map back with a uniform scale.
 // Returns kQpOptimal/kQpIterLimit (commands set), kQpInfeasible (zeroed), or
 // -1 for coincident projected points (domain_error, barrier.hpp:73-74).
-template <class Real, int L, int MP, int MO, bool FAST>
+template <class Real, int L, int MP, int MO, bool FAST, bool WARM = false>
 __device__ __forceinline__ int barrier_filter(const Grp<L>& g, BarrierRows<Real, L, MP, MO>& rows,
                                               const QpWs<Real, BarrierDesc<Real>>& ws,
                               const PhysConsts<Real>& k, bool participate, Real prx, Real pry, Real cs, Real sn,
@@ -426,7 +438,8 @@ __device__ __forceinline__ int barrier_filter(const Grp<L>& g, BarrierRows<Real,
     const bool bad = g.any(coincident);  // (the ballot also orders the row-cache writes before the QP reads)
     Grp<L>::sync();
     rows.active = 0;
-    const int status = qp_solve<Real, L, FAST>(g, rows, ws, n, participate && !bad, ux, uy, total_rows, k.tol, warm_k);
+    const int status = qp_solve<Real, L, FAST, WARM>(g, rows, ws, n, participate && !bad, ux, uy, total_rows, k.tol,
+                                                     warm_k);
     // map back + uniform scale (barrier.hpp:186-204)
     const Real mv = cs * ux + sn * uy;
     const Real mw = (-sn * ux + cs * uy) * k.inv_l;
@@ -489,20 +502,41 @@ __device__ __forceinline__ Real wrap_angle_dev(Real t) {
     return r;
 }
 
+template <class Real>
+struct Real2 {
+    Real a, b;
+};
+
+// unicycle_pose_controller (controllers.hpp:68-82): out of line, so the position
+// controller's tick loop (the benchmark path) stays small in the instruction cache.
+template <class Real>
+__device__ __noinline__ Real2<Real> pose_nominal(const PhysConsts<Real>& K, Real x, Real y, Real th, Real wpx,
+                                                 Real wpy, Real wh) {
+    Real2<Real> out{Real(0), Real(0)};
+    const Real dx = wpx - x, dy = wpy - y;
+    const Real rho = dhypot(dx, dy);
+    const Real herr = wrap_angle_dev(wh - th);
+    if (!(rho < K.pose_ptol && dabs(herr) < K.pose_htol)) {
+        const Real alpha = wrap_angle_dev(atan2(dy, dx) - th);
+        const Real beta = wrap_angle_dev(wh - th - alpha);
+        out.a = dclamp(K.k_rho * rho, -K.v_max, K.v_max);
+        out.b = dclamp(K.k_alpha * alpha + K.k_beta * beta, -K.w_max, K.w_max);
+    }
+    return out;
+}
+
 // ---------------------------------------------------------------------------
 // The fused step kernel. Persistent grid-stride loop; each warp steps 32/L
 // environments in lockstep (ghost groups past the end compute but never store).
 // ---------------------------------------------------------------------------
-// Offer the previous tick's active rows first (qp_solve warm entering order): a
-// measured per-task choice (B200, fp64). It pays where the active set is large
-// and stable (arctic_transport N=10, ~7 active rows per tick: +11 %); where
-// most ticks enter 0-2 rows the offered rows are often slack again and the
-// extra iterations cost 1-8 % (navigation ... material_transport).
+// Warm-start each tick's QP from the previous tick's active set (qp_solve WARM):
+// a measured per-task choice (B200, fp64). MRSIM_QP_WARM = 0 off, 1 arctic only,
+// 2 every task (A/B builds).
 #ifndef MRSIM_QP_WARM
 #define MRSIM_QP_WARM 1
 #endif
 __host__ __device__ constexpr bool qp_warm_order(int task) {
-    return MRSIM_QP_WARM != 0 && task == MRSIM_TASK_ARCTIC_TRANSPORT;
+    return MRSIM_QP_WARM == 2 || (MRSIM_QP_WARM == 1 && task == MRSIM_TASK_ARCTIC_TRANSPORT);
 }
 
 // First-row QP fast path (qp_solve FAST): a measured choice (B200, fp64). It
@@ -667,16 +701,10 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
             const Real pry = y + sn * p.k.l;
             // nominal command (batch.hpp:183-191, controllers.hpp:39-55, 86-92)
             Real nv = 0, nw = 0;
-            if (pose_ctl) {  // unicycle_pose_controller (controllers.hpp:68-82)
-                const Real dx = wpx - x, dy = wpy - y;
-                const Real rho = dhypot(dx, dy);
-                const Real herr = wrap_angle_dev(wth - th);
-                if (!(rho < p.k.pose_ptol && dabs(herr) < p.k.pose_htol)) {
-                    const Real alpha = wrap_angle_dev(atan2(dy, dx) - th);
-                    const Real beta = wrap_angle_dev(wth - th - alpha);
-                    nv = dclamp(p.k.k_rho * rho, -p.k.v_max, p.k.v_max);
-                    nw = dclamp(p.k.k_alpha * alpha + p.k.k_beta * beta, -p.k.w_max, p.k.w_max);
-                }
+            if (pose_ctl) {  // unicycle_pose_controller (controllers.hpp:68-82), out of line
+                const Real2<Real> c2 = pose_nominal<Real>(p.k, x, y, th, wpx, wpy, wth);
+                nv = c2.a;
+                nw = c2.b;
             } else if (!(wpx == x && wpy == y)) {
                 Real ux = p.k.k_pos * (wpx - prx);
                 Real uy = p.k.k_pos * (wpy - pry);
@@ -691,7 +719,7 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
             }
             Real cv = nv, cw = nw;
             if (c.barrier_enabled) {
-                const int bs = barrier_filter<Real, L, MP, MO, qp_fast_first_row(L)>(g, rows, sm.qp, p.k, !skip, prx, pry, cs, sn, nv, nw,
+                const int bs = barrier_filter<Real, L, MP, MO, qp_fast_first_row(L), qp_warm_order(TASK)>(g, rows, sm.qp, p.k, !skip, prx, pry, cs, sn, nv, nw,
                                                        total_rows, cv, cw, qp_warm_order(TASK) ? &warm_k : nullptr);
                 if (bs < 0 && !skip) {
                     if (lane == 0) {
