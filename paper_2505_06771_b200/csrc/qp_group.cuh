@@ -99,98 +99,89 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
         if (wmax > 0) {
             const Real ux0 = ux, uy0 = uy;
             bool wok = wk > 0;
-            // 1) S for the previous active set, one bordered-inverse update per row, in logical order
+            // 1) the previous active set on this tick's geometry: warm row j goes to physical slot j
+            //    (= its logical position), owned by lane j % L
             for (int j = 0; j < wmax; ++j) {
                 const bool act = wok && j < wk;
-                const Desc gd = rows.describe(g, act ? ws.warm[j] : rows.dummy_row());
-                Real gx, gy;
-                rows.comp(gd, lane, gx, gy);
-                if (!vl) gx = Real(0);
-                if (!vly) gy = Real(0);
-                const bool s0 = act && lp0 >= 0, s1 = act && lp1 >= 0;
-                if (s0) ws.d[q0] = rows.dot(ws.desc[q0], gd);
-                if (s1) ws.d[q1] = rows.dot(ws.desc[q1], gd);
-                Grp<L>::sync();
-                Real r0 = 0, r1 = 0;
-                if (s0) {
-                    for (unsigned m = amask; m; m &= m - 1) {
-                        const int c = __ffs(m) - 1;
-                        r0 += ws.S[q0 * n + c] * ws.d[c];
+                const int pj = act ? ws.warm[j] : rows.dummy_row();
+                const Desc gd = rows.describe(g, pj);
+                if (act) {
+                    if (lane == j % L) {
+                        ws.act[j] = pj;
+                        ws.desc[j] = gd;
+                        if (j < L) lp0 = j;
+                        else lp1 = j;
                     }
-                    ws.r[q0] = r0;
+                    if (rows.touches(gd, lane)) tm |= 1u << j;
+                    rows.set_active(g, pj, true);
                 }
-                if (s1) {
-                    for (unsigned m = amask; m; m &= m - 1) {
-                        const int c = __ffs(m) - 1;
-                        r1 += ws.S[q1 * n + c] * ws.d[c];
-                    }
-                    ws.r[q1] = r1;
-                }
-                Grp<L>::sync();
-                Real zx = gx, zy = gy;
-                if (act && vl) {
-                    for (unsigned m = tm; m; m &= m - 1) {
-                        const int c = __ffs(m) - 1;
-                        Real cx, cy;
-                        rows.comp(ws.desc[c], lane, cx, cy);
-                        zx -= ws.r[c] * cx;
-                        zy -= ws.r[c] * cy;
-                    }
-                }
-                if (!vly) zy = Real(0);
-                const Real z2 = g.sum(zx * zx + zy * zy);
-                if (act && !(z2 > Prec<Real>::eps_z)) wok = false;  // dependent now: cold start
-                if (act && wok) {  // bordered inverse (as in the inner loop's add)
-                    const Real is = Real(1) / z2;
-                    const int qk = __ffs(~amask) - 1;
-                    if (s0) {
-                        const Real ra = r0 * is;
-                        for (unsigned m = amask; m; m &= m - 1) {
-                            const int c = __ffs(m) - 1;
-                            ws.S[q0 * n + c] += ra * ws.r[c];
-                        }
-                        ws.S[q0 * n + qk] = -ra;
-                        ws.S[qk * n + q0] = -ra;
-                    }
-                    if (s1) {
-                        const Real ra = r1 * is;
-                        for (unsigned m = amask; m; m &= m - 1) {
-                            const int c = __ffs(m) - 1;
-                            ws.S[q1 * n + c] += ra * ws.r[c];
-                        }
-                        ws.S[q1 * n + qk] = -ra;
-                        ws.S[qk * n + q1] = -ra;
-                    }
-                    if (lane == (qk & (L - 1))) {
-                        ws.S[qk * n + qk] = is;
-                        ws.act[qk] = ws.warm[j];
-                        ws.desc[qk] = gd;
-                        if (qk < L) lp0 = k;
-                        else lp1 = k;
-                    }
-                    if (rows.touches(gd, lane)) tm |= 1u << qk;
-                    amask |= 1u << qk;
-                    rows.set_active(g, ws.warm[j], true);
-                    ++k;
-                }
-                Grp<L>::sync();
             }
+            if (wok) {
+                k = wk;
+                amask = (k >= 32) ? ~0u : ((1u << k) - 1u);
+            }
+            Grp<L>::sync();
+            //    M = N^T N of the set (each owner its rows), then S = M^-1 in place by Gauss-Jordan in
+            //    logical order: M is SPD and the j-th pivot is the Schur complement |z|^2 the bordered
+            //    update of row j would see, so `pivot <= eps_z` is the cold path's dependence test
+            const bool w0 = wok && lp0 >= 0, w1 = wok && lp1 >= 0;
+            if (w0)
+                for (unsigned m = amask; m; m &= m - 1) {
+                    const int c = __ffs(m) - 1;
+                    ws.S[q0 * n + c] = rows.dot(ws.desc[q0], ws.desc[c]);
+                }
+            if (w1)
+                for (unsigned m = amask; m; m &= m - 1) {
+                    const int c = __ffs(m) - 1;
+                    ws.S[q1 * n + c] = rows.dot(ws.desc[q1], ws.desc[c]);
+                }
+            for (int pv = 0; pv < wmax; ++pv) {
+                Grp<L>::sync();
+                const bool act = wok && pv < wk;
+                const Real piv = act ? ws.S[pv * n + pv] : Real(1);
+                if (act && !(piv > Prec<Real>::eps_z)) wok = false;  // dependent now: cold start
+                const bool go = act && wok;
+                if (go && lane == pv % L) {  // scale the pivot row
+                    const Real ip = Real(1) / piv;
+                    for (unsigned m = amask; m; m &= m - 1) {
+                        const int c = __ffs(m) - 1;
+                        ws.S[pv * n + c] = (c == pv) ? ip : ws.S[pv * n + c] * ip;
+                    }
+                }
+                Grp<L>::sync();
+                if (go) {  // eliminate the pivot column from the other rows
+                    if (w0 && q0 != pv) {
+                        const Real f = ws.S[q0 * n + pv];
+                        for (unsigned m = amask; m; m &= m - 1) {
+                            const int c = __ffs(m) - 1;
+                            ws.S[q0 * n + c] = (c == pv) ? -f * ws.S[pv * n + pv] : ws.S[q0 * n + c] - f * ws.S[pv * n + c];
+                        }
+                    }
+                    if (w1 && q1 != pv) {
+                        const Real f = ws.S[q1 * n + pv];
+                        for (unsigned m = amask; m; m &= m - 1) {
+                            const int c = __ffs(m) - 1;
+                            ws.S[q1 * n + c] = (c == pv) ? -f * ws.S[pv * n + pv] : ws.S[q1 * n + c] - f * ws.S[pv * n + c];
+                        }
+                    }
+                }
+            }
+            Grp<L>::sync();
             // 2) lam = S (N^T u_nom - h), u = u_nom - N lam
             rows.publish_u(lane, ux0, uy0);
             Grp<L>::sync();
-            const bool w0 = wok && lp0 >= 0, w1 = wok && lp1 >= 0;
             if (w0) ws.d[q0] = rows.dot_u(ws.desc[q0]) - rows.rhs(ws.desc[q0]);
             if (w1) ws.d[q1] = rows.dot_u(ws.desc[q1]) - rows.rhs(ws.desc[q1]);
             Grp<L>::sync();
             Real l0 = 0, l1 = 0;
-            if (w0) {
+            if (w0 && wok) {
                 for (unsigned m = amask; m; m &= m - 1) {
                     const int c = __ffs(m) - 1;
                     l0 += ws.S[q0 * n + c] * ws.d[c];
                 }
                 ws.lam[q0] = l0;
             }
-            if (w1) {
+            if (w1 && wok) {
                 for (unsigned m = amask; m; m &= m - 1) {
                     const int c = __ffs(m) - 1;
                     l1 += ws.S[q1 * n + c] * ws.d[c];
@@ -198,7 +189,7 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
                 ws.lam[q1] = l1;
             }
             // 3) dual feasibility of the warm point, else the cold start
-            if (g.any((w0 && l0 < Real(0)) || (w1 && l1 < Real(0)))) wok = false;
+            if (g.any((w0 && wok && l0 < Real(0)) || (w1 && wok && l1 < Real(0)))) wok = false;
             Grp<L>::sync();
             if (wok) {
                 for (unsigned m = tm; m; m &= m - 1) {
