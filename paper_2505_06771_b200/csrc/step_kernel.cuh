@@ -178,7 +178,12 @@ struct BarrierRows {
     Real cap;
     int nob;
     int oslot[MO1];
-    Real ocx[MO1], ocy[MO1], or2[MO1];
+    // obstacle centres (x, y) by slot (stride ostride), radii by slot (+ oinfl) or one radius^2 for all
+    const double* oxy;
+    const double* orad;
+    int ostride;
+    double oinfl;
+    Real or2u;
     unsigned active;
     bool valid;  // this lane carries a robot
 
@@ -358,6 +363,11 @@ __device__ __forceinline__ void init_rows(BarrierRows<Real, L, MP, MO>& rows, Re
     rows.valid = lane < N;
     rows.nob = 0;
     rows.npair = 0;
+    rows.oxy = nullptr;
+    rows.orad = nullptr;
+    rows.ostride = 2;
+    rows.oinfl = 0.0;
+    rows.or2u = Real(0);
 #pragma unroll
     for (int s = 0; s < MP; ++s) {
         const int pidx = lane + s * L;
@@ -422,12 +432,18 @@ __device__ __forceinline__ int barrier_filter(const Grp<L>& g, BarrierRows<Real,
 #pragma unroll
         for (int t = 0; t < BarrierRows<Real, L, MP, MO>::MO1; ++t) {
             if (t < rows.nob) {
-                const Real dx = prx - rows.ocx[t], dy = pry - rows.ocy[t];
-                const Real h = dx * dx + dy * dy - rows.or2[t];
-                const Real nrm = dsqrt(Real(4) * dx * dx + Real(4) * dy * dy);
+                const int o = rows.oslot[t] * rows.ostride;
+                Real or2 = rows.or2u;
+                if (rows.orad) {
+                    const double r = rows.orad[o] + rows.oinfl;
+                    or2 = Real(r * r);
+                }
+                const Real dx = prx - Real(rows.oxy[o]), dy = pry - Real(rows.oxy[o + 1]);
+                const Real h = dx * dx + dy * dy - or2;
+                const Real n2 = Real(4) * dx * dx + Real(4) * dy * dy;  // |row|^2 (fold_rows qp.hpp:104-125)
                 const Real gh = k.gamma * h * h * h;
-                const bool zero = nrm < Real(1e-14);
-                const Real inv = zero ? Real(0) : Real(1) / nrm;
+                const bool zero = n2 < Real(1e-28);                     // |row| < 1e-14
+                const Real inv = zero ? Real(0) : rsqrt(n2);
                 const int f = 3 * MP + 4 + 3 * t;
                 rows.F(f, lane) = Real(-2) * dx * inv;
                 rows.F(f + 1, lane) = Real(-2) * dy * inv;
@@ -580,6 +596,8 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
     BarrierRows<Real, L, MP, MO> rows;
     __shared__ unsigned char pair_tab[MRSIM_MAX_ROBOTS * (MRSIM_MAX_ROBOTS - 1)];
     init_rows(rows, sm.rc, pair_tab, lane, N, p.k.cap);
+    rows.oxy = c.layout.rware_slots;  // rware shelves: one inflated radius (barrier.hpp:157)
+    rows.or2u = p.k.obs_r_eff2;
     const int total_rows_base = rows.P + 4 * N + 4 * N;
     __shared__ double het_flat[MRSIM_MAX_ROBOTS * MRSIM_MAX_HET_COLS];  // het_augment, full team, feature order
     for (int k = threadIdx.x; k < c.het_rows * c.het_cols; k += blockDim.x) het_flat[k] = c.het[k / c.het_cols][k % c.het_cols];
@@ -676,9 +694,6 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
                         for (int t = 0; t < BarrierRows<Real, L, MP, MO>::MO1; ++t)
                             if (t == cnt) {
                                 rows.oslot[t] = o;
-                                rows.ocx[t] = Real(c.layout.rware_slots[2 * o]);
-                                rows.ocy[t] = Real(c.layout.rware_slots[2 * o + 1]);
-                                rows.or2[t] = p.k.obs_r_eff2;
                             }
                         ++cnt;
                     }

@@ -118,24 +118,22 @@ __global__ void __launch_bounds__(128) barrier_batch_kernel(const __grid_constan
         BarrierRows<Real, L, MP, MO> rows;
         __shared__ unsigned char pair_tab[MRSIM_MAX_ROBOTS * (MRSIM_MAX_ROBOTS - 1)];
         init_rows(rows, rcache, pair_tab, lane, N, k.cap);
+        rows.oxy = obstacles + t * nobs * 3;  // (x, y, r) per obstacle
+        rows.orad = rows.oxy + 2;
+        rows.ostride = 3;
+        rows.oinfl = c.projection_distance + c.discrete_margin;
         // static obstacles with masks (barrier.hpp:106-119), radius inflated (barrier.hpp:157)
         int obs_rows = 0;
-        const double infl = c.projection_distance + c.discrete_margin;
         for (int o = 0; o < nobs; ++o) {
             const uint64_t mk = masks ? masks[t * nobs + o] : 0ull;
             for (int i = 0; i < N; ++i) {
                 if (mk != 0 && ((mk >> i) & 1ull) == 0) continue;
                 ++obs_rows;
                 if (vl && i == ri) {
-                    const double* ob = obstacles + (t * nobs + o) * 3;
-                    const double r = ob[2] + infl;
 #pragma unroll
                     for (int q = 0; q < MO; ++q)
                         if (q == rows.nob) {
                             rows.oslot[q] = o;
-                            rows.ocx[q] = Real(ob[0]);
-                            rows.ocy[q] = Real(ob[1]);
-                            rows.or2[q] = Real(r * r);
                         }
                     ++rows.nob;
                 }
