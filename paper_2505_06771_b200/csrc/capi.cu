@@ -262,7 +262,7 @@ cudaError_t policy_launch(mrsim_ctx* ctx, const DevState<Real>& st, int8_t* out,
     int maxw = ctx->D;
     for (int l = 0; l < ctx->net.num_layers; ++l) maxw = maxw > ctx->net.out[l] ? maxw : ctx->net.out[l];
     p.maxw = maxw;
-    p.warp_bytes = mrsim_dev::policy_warp_bytes<Real>(ctx->N, maxw);
+    p.tile_envs = 0;  // set by the launcher
     p.num_sms = ctx->num_sms;
     p.actions = out;
     return dispatch_policy<Real>(ctx->cfg.task, p, s);

@@ -2,12 +2,15 @@
 actions that change every step): device step alone, host step without / with
 outputs, raw pinned D2H of the obs block."""
 import ctypes
+import os
+import sys
 import time
 
 import numpy as np
 import torch
 
-import paper_2505_06771_b200 as m
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2505_06771_b200 as m  # noqa: E402
 
 cfg = m.make_default_config("navigation")
 cfg.set_num_robots(4)
@@ -47,3 +50,5 @@ src = torch.empty((B, 4, cfg.obs_dim), dtype=torch.float32, device="cuda")
 dst = torch.empty((B, 4, cfg.obs_dim), dtype=torch.float32).pin_memory()
 print("pinned D2H 5.2 MB         %.1f us" % t(lambda: (dst.copy_(src, non_blocking=True), torch.cuda.synchronize())))
 print("sync only                 %.1f us" % t(lambda: gb.sync()))
+print("device step + sync each   %.1f us" % t(lambda: (gb.step(da[nxt()]), gb.sync())))
+print("device step, obs to dev, + 5.2 MB D2H + sync  %.1f us" % t(lambda: (gb.step(da[nxt()]), dst.copy_(gb._obs, non_blocking=True), gb.sync())))
