@@ -20,6 +20,12 @@ using mrsim_dev::EnvStats;
 using mrsim_dev::ResetParams;
 using mrsim_dev::StepParams;
 
+// Warp-staged obs stores on the device-buffer path too (not only for zero-copy host buffers):
+// measured -3.7 % nav N=4, neutral elsewhere (profiles/r02/ab_obs_stage.log), so off.
+#ifndef MRSIM_STAGE_DEVICE_OBS
+#define MRSIM_STAGE_DEVICE_OBS 0
+#endif
+
 struct mrsim_ctx {
     mrsim_cfg cfg;
     int device = 0;
@@ -405,7 +411,7 @@ int do_step(mrsim_ctx* ctx, DevState<Real>* s, const int8_t* actions, float* obs
     StepParams<Real> p = step_params<Real>(ctx, s, actions, obs, reward, done, next_obs, reward64, actions32);
     // warp-staged obs stores only where they pay: obs going straight to pinned host memory
     // (device-memory obs: ~2 % slower staged, measured)
-    p.obs_stage = (stage_obs || ctx->L == 1) ? ctx->obs_stage : 0;
+    p.obs_stage = (stage_obs || ctx->L == 1 || MRSIM_STAGE_DEVICE_OBS) ? ctx->obs_stage : 0;
     const int smem = ctx->smem_group * (ctx->block / ctx->L) + 4 * p.obs_stage * (ctx->block / 32);
     cudaError_t e = dispatch_step<Real>(ctx->cfg.task, p, ctx->var, ctx->grid, ctx->block, smem, stream);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "step kernel launch");
@@ -902,7 +908,7 @@ int mrsim_create(const mrsim_cfg* cfg, int device, int64_t num_envs, uint32_t fl
     // Warp-staged observation stores (one contiguous block per warp, full-line writes; what makes
     // zero-copy obs to pinned host memory efficient): on when it costs no occupancy.
     {
-        const int stage = (32 / ctx->L) * ctx->N * ctx->D;  // floats per warp
+        const int stage = (((32 / ctx->L) * ctx->N * ctx->D + 3) / 4) * 4;  // floats per warp (16-B multiple)
         const int smem2 = smem + 4 * stage * (ctx->block / 32);
         int bps2 = 0;
         e = ctx->fp64 ? dispatch_occ<double>(cfg->task, ctx->var, ctx->block, smem2, &bps2)

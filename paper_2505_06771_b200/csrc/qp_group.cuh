@@ -33,6 +33,20 @@ namespace mrsim_dev {
 
 enum QpStatusDev : int { kQpOptimal = 0, kQpInfeasible = 1, kQpIterLimit = 2 };
 
+// Diagnostic counters (builds with -DMRSIM_QP_STATS only): [0] solves, [1] warm attempts,
+// [2] warm fallbacks (dependent), [3] warm fallbacks (negative multiplier), [4] outer iterations.
+#ifdef MRSIM_QP_STATS
+__device__ unsigned long long g_qp_stats[8];
+#define MRSIM_QP_STAT(i, cond) \
+    do {                          \
+        if (cond) atomicAdd(&g_qp_stats[i], 1ull); \
+    } while (0)
+#else
+#define MRSIM_QP_STAT(i, cond) \
+    do {                          \
+    } while (0)
+#endif
+
 
 // Shared-memory workspace of one group for n variables, indexed by PHYSICAL
 // slot: S[q*n + q'] inverse Gram, lam, r, d, act (row id), desc (row descriptor).
@@ -189,7 +203,12 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
                 ws.lam[q1] = l1;
             }
             // 3) dual feasibility of the warm point, else the cold start
-            if (g.any((w0 && wok && l0 < Real(0)) || (w1 && wok && l1 < Real(0)))) wok = false;
+            MRSIM_QP_STAT(1, lane == 0 && wk > 0);
+            MRSIM_QP_STAT(2, lane == 0 && wk > 0 && !wok);
+            if (g.any((w0 && wok && l0 < Real(0)) || (w1 && wok && l1 < Real(0)))) {
+                MRSIM_QP_STAT(3, lane == 0 && wok);
+                wok = false;
+            }
             Grp<L>::sync();
             if (wok) {
                 for (unsigned m = tm; m; m &= m - 1) {
@@ -440,6 +459,7 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
             Grp<L>::sync();
         }
         if (act && !added) done = true;  // stall (qp.hpp:331-334) or infeasible
+        MRSIM_QP_STAT(4, act && lane == 0);
         if (act) ++iter;
     }
     if constexpr (WARM) {  // remember this solve's active rows, in logical order
@@ -448,6 +468,7 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
         *warm_k = (participate && status == kQpOptimal) ? k : 0;
         Grp<L>::sync();
     }
+    MRSIM_QP_STAT(0, participate && lane == 0);
     return status;
 }
 

@@ -838,7 +838,8 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
         const int ND = N * p.D;
         if (p.obs && p.obs_stage) {
             // the warp's G envs are consecutive: stage their obs, then store one contiguous block
-            // (every store instruction writes 128 contiguous bytes)
+            // (float4 stores when the block is 16-byte aligned: every store instruction writes
+            // 512 contiguous bytes; else 128)
             float* wst = reinterpret_cast<float*>(smem_raw + gpb * p.smem_bytes_per_group) +
                          (threadIdx.x >> 5) * p.obs_stage;
             float* mine = wst + (gib & (G - 1)) * ND;
@@ -850,7 +851,13 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
             const long long left = p.e_end - e0;
             const int total = static_cast<int>(left < G ? left : G) * ND;
             float* dst = p.obs + e0 * ND;
-            for (int k = threadIdx.x & 31; k < total; k += 32) dst[k] = wst[k];
+            if (((e0 * ND) & 3) == 0 && (total & 3) == 0) {
+                const float4* src4 = reinterpret_cast<const float4*>(wst);
+                float4* dst4 = reinterpret_cast<float4*>(dst);
+                for (int k = threadIdx.x & 31; k < total / 4; k += 32) dst4[k] = src4[k];
+            } else {
+                for (int k = threadIdx.x & 31; k < total; k += 32) dst[k] = wst[k];
+            }
             __syncwarp();
         } else if (p.obs && !skip) {
             float* o = p.obs + e * ND;
