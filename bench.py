@@ -347,7 +347,8 @@ def main():
         import torch.distributed as dist
 
         if backend == "nccl":
-            os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator / NVLS lines on stderr
+            os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator / NVLS lines ...
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # ... on stderr: stdout is the JSON line
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
