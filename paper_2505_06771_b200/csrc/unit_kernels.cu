@@ -250,15 +250,14 @@ int mrsim_qp_solve_batch(int device, int fp64, int count, int n, int m, const do
         return MRSIM_E_INVALID_ARGUMENT;
     if (cudaSetDevice(device) != cudaSuccess) return MRSIM_E_CUDA;
     DevBuf dA, db, dlo, dhi, du, dout, dst, dit;
-    cudaError_t e = cudaSuccess;
-    if ((e = upload(dA, A, static_cast<size_t>(count) * m * n)) != cudaSuccess) return MRSIM_E_CUDA;
-    if ((e = upload(db, b, static_cast<size_t>(count) * m)) != cudaSuccess) return MRSIM_E_CUDA;
-    if ((e = upload(dlo, lo, static_cast<size_t>(count) * n)) != cudaSuccess) return MRSIM_E_CUDA;
-    if ((e = upload(dhi, hi, static_cast<size_t>(count) * n)) != cudaSuccess) return MRSIM_E_CUDA;
-    if ((e = upload(du, u_nom, static_cast<size_t>(count) * n)) != cudaSuccess) return MRSIM_E_CUDA;
-    if ((e = upload<double>(dout, nullptr, static_cast<size_t>(count) * n)) != cudaSuccess) return MRSIM_E_CUDA;
-    if ((e = upload<int32_t>(dst, nullptr, count)) != cudaSuccess) return MRSIM_E_CUDA;
-    if ((e = upload<int32_t>(dit, nullptr, count)) != cudaSuccess) return MRSIM_E_CUDA;
+    if ((upload(dA, A, static_cast<size_t>(count) * m * n)) != cudaSuccess) return MRSIM_E_CUDA;
+    if ((upload(db, b, static_cast<size_t>(count) * m)) != cudaSuccess) return MRSIM_E_CUDA;
+    if ((upload(dlo, lo, static_cast<size_t>(count) * n)) != cudaSuccess) return MRSIM_E_CUDA;
+    if ((upload(dhi, hi, static_cast<size_t>(count) * n)) != cudaSuccess) return MRSIM_E_CUDA;
+    if ((upload(du, u_nom, static_cast<size_t>(count) * n)) != cudaSuccess) return MRSIM_E_CUDA;
+    if ((upload<double>(dout, nullptr, static_cast<size_t>(count) * n)) != cudaSuccess) return MRSIM_E_CUDA;
+    if ((upload<int32_t>(dst, nullptr, count)) != cudaSuccess) return MRSIM_E_CUDA;
+    if ((upload<int32_t>(dit, nullptr, count)) != cudaSuccess) return MRSIM_E_CUDA;
     const size_t smem_d = 2 * static_cast<size_t>(mrsim_dev::qp_slot_bytes<double>(n, m));
     const size_t smem_f = 2 * static_cast<size_t>(mrsim_dev::qp_slot_bytes<float>(n, m));
     if (smem_d > 48 * 1024)
