@@ -276,7 +276,7 @@ int mrsim_qp_solve_batch(int device, int fp64, int count, int n, int m, const do
             count, n, m, static_cast<double*>(dA.p), static_cast<double*>(db.p), static_cast<double*>(dlo.p),
             static_cast<double*>(dhi.p), static_cast<double*>(du.p), tolerance, static_cast<double*>(dout.p),
             static_cast<int32_t*>(dst.p), static_cast<int32_t*>(dit.p));
-    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return MRSIM_E_CUDA;
+    if (cudaDeviceSynchronize() != cudaSuccess) return MRSIM_E_CUDA;
     cudaMemcpy(u_out, dout.p, sizeof(double) * count * n, cudaMemcpyDeviceToHost);
     cudaMemcpy(status_out, dst.p, sizeof(int32_t) * count, cudaMemcpyDeviceToHost);
     if (iterations_out) cudaMemcpy(iterations_out, dit.p, sizeof(int32_t) * count, cudaMemcpyDeviceToHost);
