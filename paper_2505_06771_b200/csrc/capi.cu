@@ -269,6 +269,7 @@ cudaError_t policy_launch(mrsim_ctx* ctx, const DevState<Real>& st, int8_t* out,
     for (int l = 0; l < ctx->net.num_layers; ++l) maxw = maxw > ctx->net.out[l] ? maxw : ctx->net.out[l];
     p.maxw = maxw;
     p.tile_envs = 0;  // set by the launcher
+    p.warp_bytes = 0;
     p.num_sms = ctx->num_sms;
     p.actions = out;
     return dispatch_policy<Real>(ctx->cfg.task, p, s);

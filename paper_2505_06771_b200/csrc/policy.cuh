@@ -2,7 +2,9 @@
 // actions (Policy::act with PolicyKind::FeedforwardFile, policy.hpp:445-480;
 // FeedforwardWeights::forward, policy.hpp:95-116; harness.hpp:238-252).
 //
-// A block owns a tile of consecutive environments (~64 robots): it stages
+// Teams of <= 4 robots: one warp per environment (lanes own (robot, neuron) outputs,
+// four independent accumulation chains). Larger teams: a block owns a tile of
+// consecutive environments (~32 robots): it stages
 // their state in shared memory, assembles every robot's observation (the same
 // features the step kernel stores, unrounded, in the state precision) as the
 // rows of X [robots][inputs], and runs each dense layer as a small GEMM
@@ -45,7 +47,8 @@ struct PolicyParams {
     long long B;
     int N, D, bdim, nf, ni;
     int maxw;          // max(D, layer widths): row stride of the activation buffers
-    int tile_envs;     // envs per block (kPolicyTileRobots / N, fewer for wide layers)
+    int tile_envs;     // tile kernel: envs per block (kPolicyTileRobots / N, fewer for wide layers)
+    int warp_bytes;    // warp kernel: dynamic shared memory per warp
     const double* wT;  // per layer [in][out]
     const double* bias;
     PolicyNet net;
@@ -78,8 +81,139 @@ __host__ __device__ inline int policy_tile_envs(int N, int maxw) {
     return envs;
 }
 
+// Warp kernel (small teams): per-warp shared memory, state staging then two activation buffers [N][maxw].
+template <class Real>
+__host__ __device__ constexpr int policy_warp_bytes(int N, int maxw) {
+    return policy_stage_bytes<Real>() + 2 * N * maxw * 8;
+}
+
+// Small teams (N <= kPolicyWarpMaxN): one warp per env, lanes own (robot, neuron) outputs with four
+// independent accumulation chains (round 1's kernel). Larger teams: the tiled GEMM below.
+// Measured crossover (profiles/r02/ab_policy_tiles.log, policy + step): navigation N=4 0.721 vs
+// 0.823 ms (warp), discovery N=6 1.344 vs 1.257 ms and MT N=10 12.70 vs 11.77 ms (tile).
+constexpr int kPolicyWarpMaxN = 4;
+
 template <class Real, int TASK>
-__global__ void __launch_bounds__(kPolicyTileThreads) policy_kernel(const __grid_constant__ PolicyParams<Real> p) {
+__global__ void __launch_bounds__(32 * kPolicyWarps) policy_warp_kernel(const __grid_constant__ PolicyParams<Real> p) {
+    extern __shared__ __align__(16) unsigned char pol_smem[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    unsigned char* base = pol_smem + wib * p.warp_bytes;
+    PolicyStage<Real>& sm = *reinterpret_cast<PolicyStage<Real>*>(base);
+    double* bufs = reinterpret_cast<double*>(base + ((static_cast<int>(sizeof(PolicyStage<Real>)) + 15) & ~15));
+    const mrsim_cfg& c = p.c;
+    const int N = p.N, W = p.maxw;
+    if (lane == 0) arctic_drones(c, sm.drones);
+    const EnvView<Real> view{sm.xs, sm.ys, sm.ts, sm.tf, sm.ti, N, sm.drones, nullptr};
+    const long long stride = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
+    for (long long e = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + wib; e < p.B; e += stride) {
+        __syncwarp();
+        if (lane < N) {
+            sm.xs[lane] = p.s.px[e * N + lane];
+            sm.ys[lane] = p.s.py[e * N + lane];
+            sm.ts[lane] = p.s.pt[e * N + lane];
+        }
+        for (int f = lane; f < p.nf; f += 32) sm.tf[f] = p.s.tf[static_cast<long long>(f) * p.B + e];
+        for (int w = lane; w < p.ni; w += 32) sm.ti[w] = p.s.ti[static_cast<long long>(w) * p.B + e];
+        const int step = p.s.step_index[e];
+        const uint64_t pkey = p.s.pkey[e];
+        __syncwarp();
+        // every robot's observation (assemble_observations, batch.hpp:143-151), unrounded
+        double* x = bufs;
+        double* y = bufs + N * W;
+        for (int q = lane; q < N * p.D; q += 32) {
+            const int r = q / p.D, f = q - r * p.D;
+            x[r * W + f] = double(obs_feature<TASK, Real>(c, view, r, f, p.bdim));
+        }
+        __syncwarp();
+        // FeedforwardWeights::forward (policy.hpp:95-116) for all robots at once: a lane owns
+        // (robot, neuron) outputs and runs up to four of them as independent accumulation chains
+        for (int l = 0; l < p.net.num_layers; ++l) {
+            const int nin = p.net.in[l], nout = p.net.out[l], act = p.net.act[l];
+            const double* Wt = p.wT + p.net.w_off[l];
+            const double* bb = p.bias + p.net.b_off[l];
+            const int total = N * nout;
+            for (int b0 = lane; b0 < total; b0 += 128) {
+                int ro[4], oo[4];
+                double acc[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int idx = b0 + 32 * u;
+                    const int idc = idx < total ? idx : b0;
+                    ro[u] = idc / nout;
+                    oo[u] = idc - ro[u] * nout;
+                    acc[u] = __ldg(bb + oo[u]);
+                }
+                // chains live in this pass (warp-uniform): a small last layer (nav: 4 robots x 5
+                // actions = 20 outputs) needs one, not four
+                const int live = total - (b0 - lane);
+                if (live > 96 && nout == 32) {
+                    // chain u is robot 4k+u, neuron `lane`: one weight serves all four chains
+                    for (int i = 0; i < nin; ++i) {
+                        const double w = __ldg(Wt + static_cast<long long>(i) * 32 + lane);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) acc[u] = __dadd_rn(acc[u], __dmul_rn(w, x[ro[u] * W + i]));
+                    }
+                } else if (live > 96) {
+                    for (int i = 0; i < nin; ++i) {
+                        const double* wrow = Wt + static_cast<long long>(i) * nout;
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            acc[u] = __dadd_rn(acc[u], __dmul_rn(__ldg(wrow + oo[u]), x[ro[u] * W + i]));
+                    }
+                } else {
+                    for (int i = 0; i < nin; ++i) {
+                        const double* wrow = Wt + static_cast<long long>(i) * nout;
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (32 * u < live)
+                                acc[u] = __dadd_rn(acc[u], __dmul_rn(__ldg(wrow + oo[u]), x[ro[u] * W + i]));
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    double v = acc[u];
+                    if (act == MRSIM_ACT_RELU) v = v > 0 ? v : 0.0;
+                    else if (act == MRSIM_ACT_TANH) v = tanh(v);
+                    if (b0 + 32 * u < total) y[ro[u] * W + oo[u]] = v;
+                }
+            }
+            __syncwarp();
+            double* t = x;
+            x = y;
+            y = t;
+        }
+        if (lane < N) {  // Policy::act (policy.hpp:456-480), lane r for robot r
+            const double* lg = x + lane * W;
+            int a = 0;
+            if (p.net.greedy) {
+                for (int k = 1; k < 5; ++k)
+                    if (lg[k] > lg[a]) a = k;
+            } else {
+                double mx = lg[0];
+                for (int k = 0; k < 5; ++k) mx = mx < lg[k] ? lg[k] : mx;  // std::max
+                double pr[5], z = 0.0;
+                for (int k = 0; k < 5; ++k) {
+                    pr[k] = exp(__dsub_rn(lg[k], mx));
+                    z = __dadd_rn(z, pr[k]);
+                }
+                Rng rng{fork_key(fork_key(pkey, static_cast<uint64_t>(step)), static_cast<uint64_t>(lane)), 0};
+                double u = __dmul_rn(rng.uniform(), z);
+                a = 4;
+                for (int k = 0; k < 5; ++k) {
+                    u = __dsub_rn(u, pr[k]);
+                    if (u <= 0.0) {
+                        a = k;
+                        break;
+                    }
+                }
+            }
+            p.actions[e * N + lane] = static_cast<int8_t>(a);
+        }
+    }
+}
+
+template <class Real, int TASK>
+__global__ void __launch_bounds__(kPolicyTileThreads) policy_tile_kernel(const __grid_constant__ PolicyParams<Real> p) {
     extern __shared__ __align__(16) unsigned char pol_smem[];
     const mrsim_cfg& c = p.c;
     const int N = p.N, W = p.maxw, D = p.D;

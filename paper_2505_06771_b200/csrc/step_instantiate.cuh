@@ -134,11 +134,32 @@ cudaError_t launch_reset<double, MRSIM_TASK_ID>(const mrsim_dev::ResetParams<dou
 
 template <class Real>
 static cudaError_t launch_policy_any(const mrsim_dev::PolicyParams<Real>& p, cudaStream_t s) {
+    if (p.N <= mrsim_dev::kPolicyWarpMaxN) {  // one warp per env
+        mrsim_dev::PolicyParams<Real> q = p;
+        q.warp_bytes = mrsim_dev::policy_warp_bytes<Real>(p.N, p.maxw);
+        int warps = mrsim_dev::kPolicyWarps;  // fewer warps per block when one env's buffers are large
+        while (warps > 1 && warps * q.warp_bytes > 200 * 1024) warps >>= 1;
+        const long long want = (p.B + warps - 1) / warps;
+        const int smem = warps * q.warp_bytes;
+        auto k = mrsim_dev::policy_warp_kernel<Real, MRSIM_TASK_ID>;
+        if (smem > 48 * 1024) {
+            const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (e != cudaSuccess) return e;
+        }
+        // grid-stride over envs: one full wave of resident blocks on this device
+        int bps = 0;
+        const cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, 32 * warps, smem);
+        if (oe != cudaSuccess) return oe;
+        const long long full = static_cast<long long>(p.num_sms) * (bps > 0 ? bps : 1);
+        const unsigned grid = static_cast<unsigned>(want < full ? want : full);
+        k<<<grid, 32 * warps, smem, s>>>(q);
+        return cudaGetLastError();
+    }
     mrsim_dev::PolicyParams<Real> q = p;
     q.tile_envs = mrsim_dev::policy_tile_envs<Real>(p.N, p.maxw);
     const int smem = mrsim_dev::policy_tile_bytes<Real>(q.tile_envs, p.N, p.maxw);
     const unsigned grid = static_cast<unsigned>((p.B + q.tile_envs - 1) / q.tile_envs);
-    auto k = mrsim_dev::policy_kernel<Real, MRSIM_TASK_ID>;
+    auto k = mrsim_dev::policy_tile_kernel<Real, MRSIM_TASK_ID>;
     if (smem > 48 * 1024) {
         const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;

@@ -37,3 +37,17 @@ def test_n10_131072_envs_sample_matches_reference(task, steps, ref):
     print(rep)
     assert rep["ok"], rep
     assert rep["waves"] == 1
+
+
+@pytest.mark.timeout(1800)
+@pytest.mark.parametrize("task,n,B,steps", [("discovery", 6, 32768, 120), ("rware", 6, 65536, 120),
+                                            ("foraging", 4, 65536, 120)])
+def test_other_baseline_configs_every_env_matches_reference(task, n, B, steps, ref):
+    """BASELINE configs[2] (discovery N=6, the per-GPU share of 262,144 envs over 8 GPUs) and
+    configs[3] (rware / foraging) at full batch: every env against the reference, across an
+    episode boundary."""
+    cfg, sp = make_cfgs(ref, task, n)
+    rep = run_full_batch(ref, cfg, sp, B, steps)
+    print(rep)
+    assert rep["ok"], rep
+    assert rep["waves"] == 1
