@@ -97,14 +97,15 @@ def test_scalar_equals_batched_on_device():
 
 @pytest.mark.parametrize("task,n", [("navigation", 4), ("discovery", 6), ("arctic_transport", 10)])
 def test_random_permutation_of_a_large_batch_is_bit_identical(task, n):
-    """Any env may land in any warp task of the persistent loop: a random permutation of 4,096
-    envs gives, per env, bit-identical states and rewards over 20 steps."""
+    """Any env may land in any warp task of the persistent loop: a random permutation of 16,384
+    envs (uploaded through the multi-threaded host state path) gives, per env, bit-identical
+    states and rewards over 20 steps."""
     cfg = m.make_default_config(task)
     if n != cfg.raw.num_robots:
         cfg.set_num_robots(n, tile_roster=cfg.raw.het_rows > 0)
     if task == "arctic_transport":
         cfg.set_layout("arctic.spawn_zone", [-1.55, -1.05, -0.9, 0.9])
-    B = 4096
+    B = 16384
     perm = np.random.default_rng(7).permutation(B)
     a = m.CudaEnvBatch(cfg, B, fp64=True)
     a.reset_seeds([m.derive_episode_seed(3, e) for e in range(B)])
