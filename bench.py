@@ -75,6 +75,8 @@ def parse():
     ap.add_argument("--policy", default="random", choices=["random", "mlp", "scripted_goal", "prey_chaser"],
                     help="on-device policy producing each step's actions (mlp: a random 64-32 relu network)")
     ap.add_argument("--no-flush", action="store_true", help="no L2 flush between timed steps (traffic windows)")
+    ap.add_argument("--rollout", type=int, default=10,
+                    help="also time fused rollouts of this many steps per launch (mrsim_rollout; 0: skip)")
     ap.add_argument("--verify", action="store_true",
                     help="after the bench, check every env of the bench batch against the reference (150 steps)")
     ap.add_argument("--dump-states", default="", help="write each rank's final env states to PATH.rank<r>.npz")
@@ -401,6 +403,41 @@ def main():
     value = world * B * a.steps / (dev_ms / 1e3)
     kernel_ms = dev_ms / a.steps
 
+    # fused rollouts (mrsim_rollout: T steps per launch, state kept on chip across them), reported
+    # beside the per-step launches; same workload, same outputs per step, L2 flushed between launches
+    rollout = None
+    if a.rollout > 1 and a.policy == "random" and not a.env_per_thread:
+        T = a.rollout
+        launches = max(2, a.steps // T)
+        ro_out = (None, torch.empty((T, B), dtype=torch.float32, device="cuda"),
+                  torch.empty((T, B), dtype=torch.uint8, device="cuda"))
+        ro_obs = torch.empty((T, B, a.robots, cfg.obs_dim), dtype=torch.float32, device="cuda")
+        batch.rollout(T, out=(ro_obs, ro_out[1], ro_out[2]))  # warm-up
+        rs = [torch.cuda.Event(enable_timing=True) for _ in range(launches)]
+        re_ = [torch.cuda.Event(enable_timing=True) for _ in range(launches)]
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for k in range(launches):
+            if not a.no_flush:
+                torch.sum(flush, dim=0, out=sink)
+            rs[k].record(stream)
+            batch.rollout(T, out=(ro_obs, ro_out[1], ro_out[2]))
+            re_[k].record(stream)
+        torch.cuda.synchronize()
+        batch.sync()
+        r_ms = torch.tensor([sum(x.elapsed_time(y) for x, y in zip(rs, re_))], dtype=torch.float64, device=rdev)
+        if dist:
+            dist.all_reduce(r_ms, op=dist.ReduceOp.MAX)
+        r_ms = float(r_ms.item())
+        rollout = {"steps_per_launch": T, "launches": launches,
+                   "value": world * B * T * launches / (r_ms / 1e3), "unit": "env-steps/s",
+                   "ms_per_env_step_of_the_batch": r_ms / (T * launches),
+                   "what": "mrsim_rollout: T fused steps per launch, bit-identical to T mrsim_step calls "
+                           "(tests/test_gpu_rollout.py); per-step obs / reward / done written; L2 flushed "
+                           "between launches"}
+        del ro_obs, ro_out
+
     # episode statistics: the only cross-GPU reduction (sum + min), multigpu.reduce_stats
     stats = reduce_stats(batch.stats(), device=rdev)
     if a.dump_states:
@@ -474,6 +511,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": a.steps * launches_per_step,
+            "rollout": rollout,
             "clocks": clk,
             "wall_s_timed_region": wall,
             "dist_backend": backend if world > 1 else None,

@@ -285,6 +285,21 @@ int mrsim_reset_episodes(mrsim_ctx* ctx, uint64_t root_seed, int64_t first_episo
  * a CUDA graph capturing mrsim_step must capture an even number of calls. */
 int mrsim_step(mrsim_ctx* ctx, const int8_t* actions_dev, float* obs_dev, float* reward_dev,
                uint8_t* done_dev, float* next_obs_dev, void* stream);
+
+/* A fused rollout: num_steps consecutive steps of every env in ONE launch, the actions drawn on
+ * device by the harness random policy (policy_stream, harness.hpp:29-34) -- the same results,
+ * bit for bit, as calling mrsim_step num_steps times with actions_dev = NULL (the on-device
+ * equivalent of run_episodes' step loop, harness.hpp:255-286, without a host round trip between
+ * steps). Each warp keeps its envs on chip across the steps, so the state crosses HBM once per
+ * rollout and the launch's drain is paid once. Outputs are step-major, each may be NULL:
+ *   obs_dev [num_steps][num_envs][N][D] fp32, reward_dev [num_steps][num_envs] fp32,
+ *   done_dev [num_steps][num_envs] uint8.
+ * Requires the random policy (no feedforward / scripted policy), no trajectory capture and the
+ * lane-group kernel (not MRSIM_FLAG_ENV_PER_THREAD): MRSIM_E_UNSUPPORTED otherwise.
+ * Errors as mrsim_step (sticky, reported by mrsim_sync); a failing rollout is rolled back
+ * as a whole, episode statistics included. */
+int mrsim_rollout(mrsim_ctx* ctx, int num_steps, float* obs_dev, float* reward_dev, uint8_t* done_dev,
+                  void* stream);
 /* The same step with HOST buffers (the reference's std::vector<int> actions
  * and StepOutput fields): H2D of actions, step, D2H of obs/reward/done, sync.
  * Transactional: on error the batch state is left as before the call

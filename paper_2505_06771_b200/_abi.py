@@ -100,6 +100,7 @@ FUNCTIONS = {
     "mrsim_reset_episodes": (ctypes.c_int, [c_void_p, ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64,
                                             c_void_p, c_void_p]),
     "mrsim_step": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "mrsim_rollout": (ctypes.c_int, [c_void_p, ctypes.c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
     "mrsim_step_host": (ctypes.c_int, [c_void_p, P(ctypes.c_int32), P(ctypes.c_float), P(ctypes.c_double),
                                        P(ctypes.c_uint8), c_void_p]),
     "mrsim_observe": (ctypes.c_int, [c_void_p, c_void_p, c_void_p]),

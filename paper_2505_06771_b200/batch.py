@@ -221,6 +221,23 @@ class CudaEnvBatch:
         self._check(lib().mrsim_step(self._h, a, ptr(obs), ptr(rew), ptr(done), ptr(nxt), _stream_handle(stream)))
         return StepOutputs(obs, rew, done, nxt)
 
+    def rollout(self, num_steps: int, want_obs: bool = True, stream=None, out=None) -> StepOutputs:
+        """num_steps fused steps with the on-device random policy in one launch (mrsim_rollout):
+        step-major outputs obs [T, B, N, D], reward [T, B], done [T, B]; bit-identical to
+        calling step(None) num_steps times."""
+        torch = _torch()
+        dev = torch.device("cuda", self.device)
+        T = int(num_steps)
+        if out is not None:
+            obs, rew, done = out
+        else:
+            obs = torch.empty((T, self.num_envs, self.N, self.D), dtype=torch.float32, device=dev) if want_obs else None
+            rew = torch.empty((T, self.num_envs), dtype=torch.float32, device=dev)
+            done = torch.empty((T, self.num_envs), dtype=torch.uint8, device=dev)
+        ptr = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
+        self._check(lib().mrsim_rollout(self._h, T, ptr(obs), ptr(rew), ptr(done), _stream_handle(stream)))
+        return StepOutputs(obs, rew, done, None)
+
     def step_host(self, actions, out=None):
         """Synchronous step with host buffers (the reference's std::vector<int> actions).
         `out` = (obs float32 [B,N,D], reward float64 [B], done uint8 [B]) reuses caller

@@ -389,6 +389,8 @@ StepParams<Real> step_params(mrsim_ctx* ctx, DevState<Real>* s, const int8_t* ac
     p.nf = ctx->nf;
     p.ni = ctx->ni;
     p.auto_reset = (ctx->flags & MRSIM_FLAG_AUTO_RESET) ? 1 : 0;
+    p.n_steps = 1;
+    p.obs_step_stride = static_cast<long long>(ctx->B) * ctx->N * ctx->D;
     p.root_seed = ctx->root_seed;
     p.episode_stride = ctx->episode_stride;
     p.smem_bytes_per_group = ctx->smem_group;
@@ -997,6 +999,39 @@ int mrsim_step(mrsim_ctx* ctx, const int8_t* actions_dev, float* obs_dev, float*
     }
     return ctx->fp64 ? do_step<double>(ctx, ctx->sd, actions_dev, obs_dev, reward_dev, done_dev, next_obs_dev, s)
                      : do_step<float>(ctx, ctx->sf, actions_dev, obs_dev, reward_dev, done_dev, next_obs_dev, s);
+}
+
+int mrsim_rollout(mrsim_ctx* ctx, int num_steps, float* obs_dev, float* reward_dev, uint8_t* done_dev,
+                  void* stream) {
+    if (!ctx || num_steps < 1) return set_err(ctx, MRSIM_E_INVALID_ARGUMENT, "rollout: num_steps must be >= 1");
+    if (!ctx->reset_done) return set_err(ctx, MRSIM_E_INVALID_ARGUMENT, "step before reset");
+    if ((ctx->flags & MRSIM_FLAG_AUTO_RESET) && !ctx->has_episodes)
+        return set_err(ctx, MRSIM_E_INVALID_ARGUMENT, "auto-reset needs mrsim_reset_episodes (episode seeds)");
+    if (ctx->ff || ctx->scripted || ctx->d_cap || ctx->L == 1)
+        return set_err(ctx, MRSIM_E_UNSUPPORTED,
+                       "rollout: the harness random policy on the lane-group kernel only, without capture");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e;
+    if (ctx->fp64) {
+        StepParams<double> p = step_params<double>(ctx, ctx->sd, nullptr, obs_dev, reward_dev, done_dev, nullptr,
+                                                   nullptr, nullptr);
+        p.n_steps = num_steps;
+        p.obs_stage = 0;  // device buffers: direct stores (the staged path's smem is not reserved here)
+        e = dispatch_step<double>(ctx->cfg.task, p, ctx->var, ctx->grid, ctx->block,
+                                  ctx->smem_group * (ctx->block / ctx->L), s);
+    } else {
+        StepParams<float> p = step_params<float>(ctx, ctx->sf, nullptr, obs_dev, reward_dev, done_dev, nullptr,
+                                                 nullptr, nullptr);
+        p.n_steps = num_steps;
+        p.obs_stage = 0;
+        e = dispatch_step<float>(ctx->cfg.task, p, ctx->var, ctx->grid, ctx->block,
+                                 ctx->smem_group * (ctx->block / ctx->L), s);
+    }
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "rollout kernel launch");
+    step_done(ctx);
+    ctx->env_steps += ctx->B * (num_steps - 1);
+    return MRSIM_OK;
 }
 
 int mrsim_sync(mrsim_ctx* ctx, void* stream) {

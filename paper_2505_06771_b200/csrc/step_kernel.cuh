@@ -67,15 +67,17 @@ struct EnvStats {
 __device__ __forceinline__ void stats_commit(const EnvStats& st, long long e, long long serial, double ret,
                                              double metric, int success, int collisions, int qp_inf,
                                              double min_dist) {
-    st.u_episodes[e] = st.episodes[e];
-    st.u_ret[e] = st.ret[e];
-    st.u_ret_sq[e] = st.ret_sq[e];
-    st.u_metric[e] = st.metric[e];
-    st.u_success[e] = st.success[e];
-    st.u_min_dist[e] = st.min_dist[e];
-    st.u_collisions[e] = st.collisions[e];
-    st.u_qp_inf[e] = st.qp_inf[e];
-    st.upd_serial[e] = serial;
+    if (st.upd_serial[e] != serial) {  // first update of this launch (a rollout may finish several episodes)
+        st.u_episodes[e] = st.episodes[e];
+        st.u_ret[e] = st.ret[e];
+        st.u_ret_sq[e] = st.ret_sq[e];
+        st.u_metric[e] = st.metric[e];
+        st.u_success[e] = st.success[e];
+        st.u_min_dist[e] = st.min_dist[e];
+        st.u_collisions[e] = st.collisions[e];
+        st.u_qp_inf[e] = st.qp_inf[e];
+        st.upd_serial[e] = serial;
+    }
     st.episodes[e] += 1;
     st.ret[e] += ret;
     st.ret_sq[e] += ret * ret;
@@ -118,6 +120,8 @@ struct StepParams {
     long long e_begin, e_end;  // env range of this launch (the host API pipelines chunks of a step)
     int N, n, P, D, bdim, nf, ni;
     int auto_reset;
+    int n_steps;               // consecutive steps per launch (1: mrsim_step; > 1: mrsim_rollout)
+    long long obs_step_stride;  // floats between consecutive steps' obs blocks (rollout outputs)
     uint64_t root_seed;
     long long episode_stride;
     int smem_bytes_per_group;
@@ -618,310 +622,319 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
         const long long e_real = e0 + (gib & (G - 1));
         const bool ghost = e_real >= p.e_end;
         const long long e = ghost ? p.e_end - 1 : e_real;
-        // ---- load ----
-        const int step_index = p.in.step_index[e];
-        const uint64_t key = p.in.key[e];
-        Real x = p.in.px[e * N + ri], y = p.in.py[e * N + ri], th = p.in.pt[e * N + ri];
-        for (int f = lane; f < p.nf; f += L) sm.tf[f] = p.in.tf[static_cast<long long>(f) * p.B + e];
-        for (int w = lane; w < p.ni; w += L) sm.ti[w] = p.in.ti[static_cast<long long>(w) * p.B + e];
-        Grp<L>::sync();
+        // mrsim_rollout: n_steps consecutive steps of the task's envs in this launch. Step 0 reads
+        // the input copy, later steps update the output copy in place (each env belongs to this
+        // group alone), so the input copy stays untouched for the rollback of a failing launch.
+        for (int s = 0; s < p.n_steps; ++s) {
+            const DevState<Real>& in = (s == 0) ? p.in : p.out;
+            float* const obs_s = p.obs ? p.obs + s * p.obs_step_stride : nullptr;
+            float* const reward_s = p.reward ? p.reward + s * p.B : nullptr;
+            uint8_t* const done_s = p.done ? p.done + s * p.B : nullptr;
+            // ---- load ----
+            const int step_index = in.step_index[e];
+            const uint64_t key = in.key[e];
+            Real x = in.px[e * N + ri], y = in.py[e * N + ri], th = in.pt[e * N + ri];
+            for (int f = lane; f < p.nf; f += L) sm.tf[f] = in.tf[static_cast<long long>(f) * p.B + e];
+            for (int w = lane; w < p.ni; w += L) sm.ti[w] = in.ti[static_cast<long long>(w) * p.B + e];
+            Grp<L>::sync();
 
-        // ---- actions (validate_actions, batch.hpp:226-237) ----
-        int act = 0;
-        if (vl)
-            act = p.actions ? static_cast<int>(p.actions[e * N + ri])
-                            : (p.actions32 ? p.actions32[e * N + ri] : policy_action(p.in.pkey[e], step_index, ri));
-        const int bad_robot = g.first(vl && (act < 0 || act >= 5));
-        const int bad_act = g.shfl(act, bad_robot < 0 ? 0 : bad_robot);
-        if (bad_robot >= 0 && lane == 0 && !ghost) {
-            report_error(p.err, e, bad_robot, kErrInvalidAction, bad_act);
-            *p.err_serial = p.serial;
-        }
-        bool skip = ghost || bad_robot >= 0;  // compute in lockstep, never store
-
-        // ---- waypoints (Scenario::waypoints + action_to_waypoint) ----
-        const uint64_t skey = fork_key(key, 1ull + static_cast<uint64_t>(step_index));  // step_stream
-        Real wpx = x, wpy = y;
-        if (TASK == MRSIM_TASK_RANDOM_WAYPOINTS) {  // actions ignored: the stored targets (random_waypoints.hpp:40-44)
-            if (vl) {
-                wpx = sm.tf[2 * ri];
-                wpy = sm.tf[2 * ri + 1];
-            }
-        } else if (vl) {
-            const Real ss = step_size_of<TASK, Real>(c, sm.ti, ri, x, y);
-            const Real dxa = (act == 3) ? Real(-1) : ((act == 4) ? Real(1) : Real(0));
-            const Real dya = (act == 1) ? Real(1) : ((act == 2) ? Real(-1) : Real(0));
-            wpx = x + dxa * ss;
-            wpy = y + dya * ss;
-            if (c.action_noise_scale > 0.0) {
-                const double half = c.action_noise_scale * static_cast<double>(ss);
-                Rng nr{skey, static_cast<uint64_t>(2 * ri)};
-                wpx += static_cast<Real>(nr.uniform(-half, half));
-                wpy += static_cast<Real>(nr.uniform(-half, half));
-            }
-            wpx = dclamp(wpx, -p.k.hw, p.k.hw);
-            wpy = dclamp(wpy, -p.k.hh, p.k.hh);
-        }
-
-        // goal headings for the pose controller (Scenario::waypoint_headings, batch.hpp:169-171)
-        const bool pose_ctl = c.controller == MRSIM_CONTROLLER_UNICYCLE_POSE;
-        Real wth = th;
-        if (pose_ctl) {
-            if (TASK == MRSIM_TASK_RANDOM_WAYPOINTS) {
-                wth = sm.tf[2 * N + ri];  // random_waypoints.hpp:46-50
-            } else {  // scenario.hpp:168-177
-                const Real ddx = wpx - x, ddy = wpy - y;
-                wth = dhypot(ddx, ddy) > Real(1e-12) ? atan2(ddy, ddx) : th;
-            }
-        }
-
-        // ---- static obstacles (Scenario::add_obstacles, rware.hpp:54-68) ----
-        int n_obs_rows = 0;
-        if (MO > 0) {
-            const int S = c.layout.rware_num_slots;
-            unsigned carriers = 0;
-            for (int i = 0; i < N; ++i) carriers |= (ti_byte(sm.ti, S + i) != 0 ? 1u : 0u) << i;
-            rows.nob = 0;
-            if (carriers != 0u) {
-                int staged = 0;
-                for (int o = 0; o < S; ++o) staged += ti_byte(sm.ti, o) != 0 ? 1 : 0;
-                n_obs_rows = staged * __popc(carriers);
-                if (vl && ((carriers >> ri) & 1u)) {
-                    int cnt = 0;
-                    for (int o = 0; o < S; ++o) {
-                        if (ti_byte(sm.ti, o) == 0) continue;
-#pragma unroll
-                        for (int t = 0; t < BarrierRows<Real, L, MP, MO>::MO1; ++t)
-                            if (t == cnt) {
-                                rows.oslot[t] = o;
-                            }
-                        ++cnt;
-                    }
-                    rows.nob = cnt;
-                }
-            }
-        }
-        const int total_rows = total_rows_base + n_obs_rows;
-
-        // ---- physics ticks ----
-        Real min_dist = p.in.min_dist[e];
-        Real min_d2 = Consts<Real>::inf;  // min squared pairwise distance over this step's ticks
-        int qp_inf = p.in.qp_inf[e];
-        bool collision = false;
-        int warm_k = 0;  // QP warm entering order: the previous tick's active rows (none at a step's first tick)
-        for (int tick = 0; tick < c.sub_steps; ++tick) {
-            Real sn, cs;
-            dsincos(th, &sn, &cs);
-            const Real prx = x + cs * p.k.l;  // projected_point (controllers.hpp:34-36)
-            const Real pry = y + sn * p.k.l;
-            // nominal command (batch.hpp:183-191, controllers.hpp:39-55, 86-92)
-            Real nv = 0, nw = 0;
-            if (pose_ctl) {  // unicycle_pose_controller (controllers.hpp:68-82), out of line
-                const Real2<Real> c2 = pose_nominal<Real>(p.k, x, y, th, wpx, wpy, wth);
-                nv = c2.a;
-                nw = c2.b;
-            } else if (!(wpx == x && wpy == y)) {
-                Real ux = p.k.k_pos * (wpx - prx);
-                Real uy = p.k.k_pos * (wpy - pry);
-                const Real nrm = dsqrt(ux * ux + uy * uy);
-                if (!(nrm <= p.k.si_max || nrm == Real(0))) {
-                    const Real sc = p.k.si_max / nrm;
-                    ux *= sc;
-                    uy *= sc;
-                }
-                nv = dclamp(cs * ux + sn * uy, -p.k.v_max, p.k.v_max);
-                nw = dclamp((-sn * ux + cs * uy) * p.k.inv_l, -p.k.w_max, p.k.w_max);
-            }
-            Real cv = nv, cw = nw;
-            if (c.barrier_enabled) {
-                const int bs = barrier_filter<Real, L, MP, MO, qp_fast_first_row(L), qp_warm_order(TASK)>(g, rows, sm.qp, p.k, !skip, prx, pry, cs, sn, nv, nw,
-                                                       total_rows, cv, cw, qp_warm_order(TASK) ? &warm_k : nullptr);
-                if (bs < 0 && !skip) {
-                    if (lane == 0) {
-                        report_error(p.err, e, 0, kErrCoincident);
-                        *p.err_serial = p.serial;
-                    }
-                    skip = true;
-                }
-                if (bs == kQpInfeasible) ++qp_inf;
-            }
-            // unicycle Euler step + wrap + arena clamp (core.hpp:112-118, batch.hpp:199-203)
-            x = x + cv * cs * p.k.dt;
-            y = y + cv * sn * p.k.dt;
-            const Real tn = th + cw * p.k.dt;
-            if (vl && !skip && !isfinite(tn)) {
-                report_error(p.err, e, ri, kErrNonFinite);
+            // ---- actions (validate_actions, batch.hpp:226-237) ----
+            int act = 0;
+            if (vl)
+                act = p.actions ? static_cast<int>(p.actions[e * N + ri])
+                                : (p.actions32 ? p.actions32[e * N + ri] : policy_action(in.pkey[e], step_index, ri));
+            const int bad_robot = g.first(vl && (act < 0 || act >= 5));
+            const int bad_act = g.shfl(act, bad_robot < 0 ? 0 : bad_robot);
+            if (bad_robot >= 0 && lane == 0 && !ghost) {
+                report_error(p.err, e, bad_robot, kErrInvalidAction, bad_act);
                 *p.err_serial = p.serial;
             }
-            th = wrap_angle_dev(tn);
-            x = dclamp(x, -p.k.hw, p.k.hw);
-            y = dclamp(y, -p.k.hh, p.k.hh);
-            // collision check (batch.hpp:204-209)
-            if (N > 1) {  // squared distances; sqrt is monotone, so it is taken once per step
-                Real md2 = Consts<Real>::inf;
-                constexpr int kU = BarrierRows<Real, L, MP, MO>::kU;  // publish the poses (smem, not shuffles)
-                Grp<L>::sync();
-                rows.F(kU, lane) = x;
-                rows.F(kU + 1, lane) = y;
-                Grp<L>::sync();
-#pragma unroll
-                for (int s = 0; s < MP; ++s) {
-                    const Real xi = rows.F(kU, rows.pi[s]), yi = rows.F(kU + 1, rows.pi[s]);
-                    const Real xj = rows.F(kU, rows.pj[s]), yj = rows.F(kU + 1, rows.pj[s]);
-                    const Real dx = xi - xj, dy = yi - yj;
-                    if (s < rows.npair) md2 = dmin(md2, dx * dx + dy * dy);
+            bool skip = ghost || bad_robot >= 0;  // compute in lockstep, never store
+
+            // ---- waypoints (Scenario::waypoints + action_to_waypoint) ----
+            const uint64_t skey = fork_key(key, 1ull + static_cast<uint64_t>(step_index));  // step_stream
+            Real wpx = x, wpy = y;
+            if (TASK == MRSIM_TASK_RANDOM_WAYPOINTS) {  // actions ignored: the stored targets (random_waypoints.hpp:40-44)
+                if (vl) {
+                    wpx = sm.tf[2 * ri];
+                    wpy = sm.tf[2 * ri + 1];
                 }
-                md2 = g.min(md2);
-                min_d2 = dmin(min_d2, md2);
-                collision = collision || md2 < p.k.coll_r2;
+            } else if (vl) {
+                const Real ss = step_size_of<TASK, Real>(c, sm.ti, ri, x, y);
+                const Real dxa = (act == 3) ? Real(-1) : ((act == 4) ? Real(1) : Real(0));
+                const Real dya = (act == 1) ? Real(1) : ((act == 2) ? Real(-1) : Real(0));
+                wpx = x + dxa * ss;
+                wpy = y + dya * ss;
+                if (c.action_noise_scale > 0.0) {
+                    const double half = c.action_noise_scale * static_cast<double>(ss);
+                    Rng nr{skey, static_cast<uint64_t>(2 * ri)};
+                    wpx += static_cast<Real>(nr.uniform(-half, half));
+                    wpy += static_cast<Real>(nr.uniform(-half, half));
+                }
+                wpx = dclamp(wpx, -p.k.hw, p.k.hw);
+                wpy = dclamp(wpy, -p.k.hh, p.k.hh);
             }
-        }
 
-        min_dist = dmin(min_dist, dsqrt(min_d2));
-        // ---- stage final poses, transition, bookkeeping (lane 0) ----
-        if (vl) {
-            sm.xs[ri] = x;
-            sm.ys[ri] = y;
-            sm.ts[ri] = th;
-        }
-        Grp<L>::sync();
-        if (lane == 0) {
-            Real metric = p.in.metric[e];
-            int success = p.in.success[e];
-            int collisions = p.in.collisions[e];
-            Real ep_return = p.in.ep_return[e];
-            // the transition continues the step stream after the waypoint noise draws
-            Rng trng{skey, (c.action_noise_scale > 0.0 && TASK != MRSIM_TASK_RANDOM_WAYPOINTS)
-                               ? static_cast<uint64_t>(2 * N) : 0ull};
-            EnvView<Real> v = view;
-            Real reward = transition_task<TASK, Real>(c, v, trng, metric);
-            if (collision) {
-                collisions += 1;
-                reward += Real(c.coef[MRSIM_COEF_VIOLATION]);
+            // goal headings for the pose controller (Scenario::waypoint_headings, batch.hpp:169-171)
+            const bool pose_ctl = c.controller == MRSIM_CONTROLLER_UNICYCLE_POSE;
+            Real wth = th;
+            if (pose_ctl) {
+                if (TASK == MRSIM_TASK_RANDOM_WAYPOINTS) {
+                    wth = sm.tf[2 * N + ri];  // random_waypoints.hpp:46-50
+                } else {  // scenario.hpp:168-177
+                    const Real ddx = wpx - x, ddy = wpy - y;
+                    wth = dhypot(ddx, ddy) > Real(1e-12) ? atan2(ddy, ddx) : th;
+                }
             }
-            const int new_step = step_index + 1;
-            const int done = new_step >= c.max_steps ? 1 : 0;
-            if (done) finalize_task<TASK, Real>(c, v, metric, success);
-            ep_return += reward;
-            misc[0] = done;
-            if (!skip) {
-                if (p.reward) p.reward[e] = static_cast<float>(reward);
-                if (p.reward64) p.reward64[e] = static_cast<double>(reward);
-                if (p.done) p.done[e] = static_cast<uint8_t>(done);
-                if (done && new_step == c.max_steps)  // EpisodeStats (harness.hpp:277-285)
-                    stats_commit(p.st, e, p.serial, static_cast<double>(ep_return), static_cast<double>(metric),
-                                 success, collisions, qp_inf, static_cast<double>(min_dist));
-                p.out.step_index[e] = new_step;
-                p.out.collisions[e] = collisions;
-                p.out.qp_inf[e] = qp_inf;
-                p.out.success[e] = success;
-                p.out.metric[e] = metric;
-                p.out.min_dist[e] = min_dist;
-                p.out.ep_return[e] = ep_return;
-                p.out.key[e] = key;
-                p.out.seed[e] = p.in.seed[e];
-                p.out.pkey[e] = p.in.pkey[e];
-                p.out.episode[e] = p.in.episode[e];
-            }
-        }
-        Grp<L>::sync();
-        const int done = misc[0];
 
-        // ---- observations (assemble_observations, batch.hpp:143-151) ----
-        if (TASK == MRSIM_TASK_ARCTIC_TRANSPORT) {  // each drone's cell once, not once per patch feature
-            if (lane < n_drones) {
-                const int d = sm.drones[lane];
-                arctic_cell<Real>(c, sm.xs[d], sm.ys[d], sm.dcell[2 * lane], sm.dcell[2 * lane + 1]);
+            // ---- static obstacles (Scenario::add_obstacles, rware.hpp:54-68) ----
+            int n_obs_rows = 0;
+            if (MO > 0) {
+                const int S = c.layout.rware_num_slots;
+                unsigned carriers = 0;
+                for (int i = 0; i < N; ++i) carriers |= (ti_byte(sm.ti, S + i) != 0 ? 1u : 0u) << i;
+                rows.nob = 0;
+                if (carriers != 0u) {
+                    int staged = 0;
+                    for (int o = 0; o < S; ++o) staged += ti_byte(sm.ti, o) != 0 ? 1 : 0;
+                    n_obs_rows = staged * __popc(carriers);
+                    if (vl && ((carriers >> ri) & 1u)) {
+                        int cnt = 0;
+                        for (int o = 0; o < S; ++o) {
+                            if (ti_byte(sm.ti, o) == 0) continue;
+#pragma unroll
+                            for (int t = 0; t < BarrierRows<Real, L, MP, MO>::MO1; ++t)
+                                if (t == cnt) {
+                                    rows.oslot[t] = o;
+                                }
+                            ++cnt;
+                        }
+                        rows.nob = cnt;
+                    }
+                }
             }
-            Grp<L>::sync();
-        }
-        const int ND = N * p.D;
-        if (p.obs && p.obs_stage) {
-            // the warp's G envs are consecutive: stage their obs, then store one contiguous block
-            // (float4 stores when the block is 16-byte aligned: every store instruction writes
-            // 512 contiguous bytes; else 128)
-            float* wst = reinterpret_cast<float*>(smem_raw + gpb * p.smem_bytes_per_group) +
-                         (threadIdx.x >> 5) * p.obs_stage;
-            float* mine = wst + (gib & (G - 1)) * ND;
-            for (int q = lane, r = lane / p.D, f = lane - (lane / p.D) * p.D; q < ND; q += L) {
-                mine[q] = static_cast<float>(obs_feature<TASK, Real>(c, view, r, f, p.bdim));
-                for (f += L; f >= p.D; f -= p.D) ++r;
-            }
-            __syncwarp();
-            const long long left = p.e_end - e0;
-            const int total = static_cast<int>(left < G ? left : G) * ND;
-            float* dst = p.obs + e0 * ND;
-            if (((e0 * ND) & 3) == 0 && (total & 3) == 0) {
-                const float4* src4 = reinterpret_cast<const float4*>(wst);
-                float4* dst4 = reinterpret_cast<float4*>(dst);
-                for (int k = threadIdx.x & 31; k < total / 4; k += 32) dst4[k] = src4[k];
-            } else {
-                for (int k = threadIdx.x & 31; k < total; k += 32) dst[k] = wst[k];
-            }
-            __syncwarp();
-        } else if (p.obs && !skip) {
-            float* o = p.obs + e * ND;
-            for (int q = lane, r = lane / p.D, f = lane - (lane / p.D) * p.D; q < ND; q += L) {
-                o[q] = static_cast<float>(obs_feature<TASK, Real>(c, view, r, f, p.bdim));
-                for (f += L; f >= p.D; f -= p.D) ++r;
-            }
-        }
+            const int total_rows = total_rows_base + n_obs_rows;
 
-        // ---- auto-reset (harness wave semantics, harness.hpp:227-232) ----
-        if (p.auto_reset && done && !skip) {
-            if (lane == 0) {
-                const long long episode = p.in.episode[e] + p.episode_stride;
-                const uint64_t seed = derive_episode_seed(p.root_seed, episode);
-                const uint64_t nkey = key_from_seed(seed);
-                ResetOut ro;
-                int bad = 0;
-                const int rerr = reset_task<TASK>(c, nkey, ro, &bad);
-                if (rerr) {
-                    report_error(p.err, e, bad, static_cast<unsigned>(rerr));
+            // ---- physics ticks ----
+            Real min_dist = in.min_dist[e];
+            Real min_d2 = Consts<Real>::inf;  // min squared pairwise distance over this step's ticks
+            int qp_inf = in.qp_inf[e];
+            bool collision = false;
+            int warm_k = 0;  // QP warm entering order: the previous tick's active rows (none at a step's first tick)
+            for (int tick = 0; tick < c.sub_steps; ++tick) {
+                Real sn, cs;
+                dsincos(th, &sn, &cs);
+                const Real prx = x + cs * p.k.l;  // projected_point (controllers.hpp:34-36)
+                const Real pry = y + sn * p.k.l;
+                // nominal command (batch.hpp:183-191, controllers.hpp:39-55, 86-92)
+                Real nv = 0, nw = 0;
+                if (pose_ctl) {  // unicycle_pose_controller (controllers.hpp:68-82), out of line
+                    const Real2<Real> c2 = pose_nominal<Real>(p.k, x, y, th, wpx, wpy, wth);
+                    nv = c2.a;
+                    nw = c2.b;
+                } else if (!(wpx == x && wpy == y)) {
+                    Real ux = p.k.k_pos * (wpx - prx);
+                    Real uy = p.k.k_pos * (wpy - pry);
+                    const Real nrm = dsqrt(ux * ux + uy * uy);
+                    if (!(nrm <= p.k.si_max || nrm == Real(0))) {
+                        const Real sc = p.k.si_max / nrm;
+                        ux *= sc;
+                        uy *= sc;
+                    }
+                    nv = dclamp(cs * ux + sn * uy, -p.k.v_max, p.k.v_max);
+                    nw = dclamp((-sn * ux + cs * uy) * p.k.inv_l, -p.k.w_max, p.k.w_max);
+                }
+                Real cv = nv, cw = nw;
+                if (c.barrier_enabled) {
+                    const int bs = barrier_filter<Real, L, MP, MO, qp_fast_first_row(L), qp_warm_order(TASK)>(g, rows, sm.qp, p.k, !skip, prx, pry, cs, sn, nv, nw,
+                                                           total_rows, cv, cw, qp_warm_order(TASK) ? &warm_k : nullptr);
+                    if (bs < 0 && !skip) {
+                        if (lane == 0) {
+                            report_error(p.err, e, 0, kErrCoincident);
+                            *p.err_serial = p.serial;
+                        }
+                        skip = true;
+                    }
+                    if (bs == kQpInfeasible) ++qp_inf;
+                }
+                // unicycle Euler step + wrap + arena clamp (core.hpp:112-118, batch.hpp:199-203)
+                x = x + cv * cs * p.k.dt;
+                y = y + cv * sn * p.k.dt;
+                const Real tn = th + cw * p.k.dt;
+                if (vl && !skip && !isfinite(tn)) {
+                    report_error(p.err, e, ri, kErrNonFinite);
                     *p.err_serial = p.serial;
                 }
-                for (int i = 0; i < N; ++i) {
-                    sm.xs[i] = static_cast<Real>(ro.x[i]);
-                    sm.ys[i] = static_cast<Real>(ro.y[i]);
-                    sm.ts[i] = static_cast<Real>(ro.th[i]);
+                th = wrap_angle_dev(tn);
+                x = dclamp(x, -p.k.hw, p.k.hw);
+                y = dclamp(y, -p.k.hh, p.k.hh);
+                // collision check (batch.hpp:204-209)
+                if (N > 1) {  // squared distances; sqrt is monotone, so it is taken once per step
+                    Real md2 = Consts<Real>::inf;
+                    constexpr int kU = BarrierRows<Real, L, MP, MO>::kU;  // publish the poses (smem, not shuffles)
+                    Grp<L>::sync();
+                    rows.F(kU, lane) = x;
+                    rows.F(kU + 1, lane) = y;
+                    Grp<L>::sync();
+#pragma unroll
+                    for (int s = 0; s < MP; ++s) {
+                        const Real xi = rows.F(kU, rows.pi[s]), yi = rows.F(kU + 1, rows.pi[s]);
+                        const Real xj = rows.F(kU, rows.pj[s]), yj = rows.F(kU + 1, rows.pj[s]);
+                        const Real dx = xi - xj, dy = yi - yj;
+                        if (s < rows.npair) md2 = dmin(md2, dx * dx + dy * dy);
+                    }
+                    md2 = g.min(md2);
+                    min_d2 = dmin(min_d2, md2);
+                    collision = collision || md2 < p.k.coll_r2;
                 }
-                for (int f = 0; f < p.nf; ++f) sm.tf[f] = static_cast<Real>(ro.tf[f]);
-                for (int w = 0; w < p.ni; ++w) sm.ti[w] = ro.ti[w];
-                p.out.step_index[e] = 0;
-                p.out.collisions[e] = 0;
-                p.out.qp_inf[e] = 0;
-                p.out.success[e] = 0;
-                p.out.metric[e] = 0;
-                p.out.min_dist[e] = Consts<Real>::inf;
-                p.out.ep_return[e] = 0;
-                p.out.key[e] = nkey;
-                p.out.seed[e] = seed;
-                p.out.pkey[e] = policy_key_of(seed);
-                p.out.episode[e] = episode;
             }
-        }
-        Grp<L>::sync();
-        if (p.auto_reset && done && !skip && p.next_obs) {
-            EnvView<Real> fresh = view;  // the drone-cell cache holds the terminal poses
-            fresh.dcell = nullptr;
-            float* o = p.next_obs + e * ND;
-            for (int q = lane; q < ND; q += L) {
-                const int r = q / p.D;
-                o[q] = static_cast<float>(obs_feature<TASK, Real>(c, fresh, r, q - r * p.D, p.bdim));
-            }
-        }
 
-        // ---- store ----
-        if (!skip) {
-            for (int i = lane; i < N; i += L) {
-                p.out.px[e * N + i] = sm.xs[i];
-                p.out.py[e * N + i] = sm.ys[i];
-                p.out.pt[e * N + i] = sm.ts[i];
+            min_dist = dmin(min_dist, dsqrt(min_d2));
+            // ---- stage final poses, transition, bookkeeping (lane 0) ----
+            if (vl) {
+                sm.xs[ri] = x;
+                sm.ys[ri] = y;
+                sm.ts[ri] = th;
             }
-            for (int f = lane; f < p.nf; f += L) p.out.tf[static_cast<long long>(f) * p.B + e] = sm.tf[f];
-            for (int w = lane; w < p.ni; w += L) p.out.ti[static_cast<long long>(w) * p.B + e] = sm.ti[w];
-        }
-        Grp<L>::sync();
+            Grp<L>::sync();
+            if (lane == 0) {
+                Real metric = in.metric[e];
+                int success = in.success[e];
+                int collisions = in.collisions[e];
+                Real ep_return = in.ep_return[e];
+                // the transition continues the step stream after the waypoint noise draws
+                Rng trng{skey, (c.action_noise_scale > 0.0 && TASK != MRSIM_TASK_RANDOM_WAYPOINTS)
+                                   ? static_cast<uint64_t>(2 * N) : 0ull};
+                EnvView<Real> v = view;
+                Real reward = transition_task<TASK, Real>(c, v, trng, metric);
+                if (collision) {
+                    collisions += 1;
+                    reward += Real(c.coef[MRSIM_COEF_VIOLATION]);
+                }
+                const int new_step = step_index + 1;
+                const int done = new_step >= c.max_steps ? 1 : 0;
+                if (done) finalize_task<TASK, Real>(c, v, metric, success);
+                ep_return += reward;
+                misc[0] = done;
+                if (!skip) {
+                    if (reward_s) reward_s[e] = static_cast<float>(reward);
+                    if (p.reward64) p.reward64[e] = static_cast<double>(reward);
+                    if (done_s) done_s[e] = static_cast<uint8_t>(done);
+                    if (done && new_step == c.max_steps)  // EpisodeStats (harness.hpp:277-285)
+                        stats_commit(p.st, e, p.serial, static_cast<double>(ep_return), static_cast<double>(metric),
+                                     success, collisions, qp_inf, static_cast<double>(min_dist));
+                    p.out.step_index[e] = new_step;
+                    p.out.collisions[e] = collisions;
+                    p.out.qp_inf[e] = qp_inf;
+                    p.out.success[e] = success;
+                    p.out.metric[e] = metric;
+                    p.out.min_dist[e] = min_dist;
+                    p.out.ep_return[e] = ep_return;
+                    p.out.key[e] = key;
+                    p.out.seed[e] = in.seed[e];
+                    p.out.pkey[e] = in.pkey[e];
+                    p.out.episode[e] = in.episode[e];
+                }
+            }
+            Grp<L>::sync();
+            const int done = misc[0];
+
+            // ---- observations (assemble_observations, batch.hpp:143-151) ----
+            if (TASK == MRSIM_TASK_ARCTIC_TRANSPORT) {  // each drone's cell once, not once per patch feature
+                if (lane < n_drones) {
+                    const int d = sm.drones[lane];
+                    arctic_cell<Real>(c, sm.xs[d], sm.ys[d], sm.dcell[2 * lane], sm.dcell[2 * lane + 1]);
+                }
+                Grp<L>::sync();
+            }
+            const int ND = N * p.D;
+            if (obs_s && p.obs_stage) {
+                // the warp's G envs are consecutive: stage their obs, then store one contiguous block
+                // (float4 stores when the block is 16-byte aligned: every store instruction writes
+                // 512 contiguous bytes; else 128)
+                float* wst = reinterpret_cast<float*>(smem_raw + gpb * p.smem_bytes_per_group) +
+                             (threadIdx.x >> 5) * p.obs_stage;
+                float* mine = wst + (gib & (G - 1)) * ND;
+                for (int q = lane, r = lane / p.D, f = lane - (lane / p.D) * p.D; q < ND; q += L) {
+                    mine[q] = static_cast<float>(obs_feature<TASK, Real>(c, view, r, f, p.bdim));
+                    for (f += L; f >= p.D; f -= p.D) ++r;
+                }
+                __syncwarp();
+                const long long left = p.e_end - e0;
+                const int total = static_cast<int>(left < G ? left : G) * ND;
+                float* dst = obs_s + e0 * ND;
+                if (((e0 * ND) & 3) == 0 && (total & 3) == 0) {
+                    const float4* src4 = reinterpret_cast<const float4*>(wst);
+                    float4* dst4 = reinterpret_cast<float4*>(dst);
+                    for (int k = threadIdx.x & 31; k < total / 4; k += 32) dst4[k] = src4[k];
+                } else {
+                    for (int k = threadIdx.x & 31; k < total; k += 32) dst[k] = wst[k];
+                }
+                __syncwarp();
+            } else if (obs_s && !skip) {
+                float* o = obs_s + e * ND;
+                for (int q = lane, r = lane / p.D, f = lane - (lane / p.D) * p.D; q < ND; q += L) {
+                    o[q] = static_cast<float>(obs_feature<TASK, Real>(c, view, r, f, p.bdim));
+                    for (f += L; f >= p.D; f -= p.D) ++r;
+                }
+            }
+
+            // ---- auto-reset (harness wave semantics, harness.hpp:227-232) ----
+            if (p.auto_reset && done && !skip) {
+                if (lane == 0) {
+                    const long long episode = in.episode[e] + p.episode_stride;
+                    const uint64_t seed = derive_episode_seed(p.root_seed, episode);
+                    const uint64_t nkey = key_from_seed(seed);
+                    ResetOut ro;
+                    int bad = 0;
+                    const int rerr = reset_task<TASK>(c, nkey, ro, &bad);
+                    if (rerr) {
+                        report_error(p.err, e, bad, static_cast<unsigned>(rerr));
+                        *p.err_serial = p.serial;
+                    }
+                    for (int i = 0; i < N; ++i) {
+                        sm.xs[i] = static_cast<Real>(ro.x[i]);
+                        sm.ys[i] = static_cast<Real>(ro.y[i]);
+                        sm.ts[i] = static_cast<Real>(ro.th[i]);
+                    }
+                    for (int f = 0; f < p.nf; ++f) sm.tf[f] = static_cast<Real>(ro.tf[f]);
+                    for (int w = 0; w < p.ni; ++w) sm.ti[w] = ro.ti[w];
+                    p.out.step_index[e] = 0;
+                    p.out.collisions[e] = 0;
+                    p.out.qp_inf[e] = 0;
+                    p.out.success[e] = 0;
+                    p.out.metric[e] = 0;
+                    p.out.min_dist[e] = Consts<Real>::inf;
+                    p.out.ep_return[e] = 0;
+                    p.out.key[e] = nkey;
+                    p.out.seed[e] = seed;
+                    p.out.pkey[e] = policy_key_of(seed);
+                    p.out.episode[e] = episode;
+                }
+            }
+            Grp<L>::sync();
+            if (p.auto_reset && done && !skip && p.next_obs) {
+                EnvView<Real> fresh = view;  // the drone-cell cache holds the terminal poses
+                fresh.dcell = nullptr;
+                float* o = p.next_obs + e * ND;
+                for (int q = lane; q < ND; q += L) {
+                    const int r = q / p.D;
+                    o[q] = static_cast<float>(obs_feature<TASK, Real>(c, fresh, r, q - r * p.D, p.bdim));
+                }
+            }
+
+            // ---- store ----
+            if (!skip) {
+                for (int i = lane; i < N; i += L) {
+                    p.out.px[e * N + i] = sm.xs[i];
+                    p.out.py[e * N + i] = sm.ys[i];
+                    p.out.pt[e * N + i] = sm.ts[i];
+                }
+                for (int f = lane; f < p.nf; f += L) p.out.tf[static_cast<long long>(f) * p.B + e] = sm.tf[f];
+                for (int w = lane; w < p.ni; w += L) p.out.ti[static_cast<long long>(w) * p.B + e] = sm.ti[w];
+            }
+            Grp<L>::sync();
+        }  // rollout steps
     }
 }
 
