@@ -408,11 +408,15 @@ def main():
     rollout = None
     if a.rollout > 1 and a.policy == "random" and not a.env_per_thread:
         T = a.rollout
-        launches = max(2, a.steps // T)
+        launches = max(1, a.steps // T)
         ro_out = (None, torch.empty((T, B), dtype=torch.float32, device="cuda"),
                   torch.empty((T, B), dtype=torch.uint8, device="cuda"))
         ro_obs = torch.empty((T, B, a.robots, cfg.obs_dim), dtype=torch.float32, device="cuda")
-        batch.rollout(T, out=(ro_obs, ro_out[1], ro_out[2]))  # warm-up
+        # a twin batch at the same episode phase as the per-step measurement: same reset, same warm-up
+        rb = m.CudaEnvBatch(cfg, B, device=local, fp64=(not a.fp32), auto_reset=True)
+        rb.reset_episodes(root_seed=0, first_episode=shard.first_episode, episode_stride=shard.episode_stride)
+        for _ in range(max(a.warmup, 3)):
+            rb.step(None)
         rs = [torch.cuda.Event(enable_timing=True) for _ in range(launches)]
         re_ = [torch.cuda.Event(enable_timing=True) for _ in range(launches)]
         if dist:
@@ -422,10 +426,11 @@ def main():
             if not a.no_flush:
                 torch.sum(flush, dim=0, out=sink)
             rs[k].record(stream)
-            batch.rollout(T, out=(ro_obs, ro_out[1], ro_out[2]))
+            rb.rollout(T, out=(ro_obs, ro_out[1], ro_out[2]))
             re_[k].record(stream)
         torch.cuda.synchronize()
-        batch.sync()
+        rb.sync()
+        rb.close()
         r_ms = torch.tensor([sum(x.elapsed_time(y) for x, y in zip(rs, re_))], dtype=torch.float64, device=rdev)
         if dist:
             dist.all_reduce(r_ms, op=dist.ReduceOp.MAX)
@@ -434,8 +439,9 @@ def main():
                    "value": world * B * T * launches / (r_ms / 1e3), "unit": "env-steps/s",
                    "ms_per_env_step_of_the_batch": r_ms / (T * launches),
                    "what": "mrsim_rollout: T fused steps per launch, bit-identical to T mrsim_step calls "
-                           "(tests/test_gpu_rollout.py); per-step obs / reward / done written; L2 flushed "
-                           "between launches"}
+                           "(tests/test_gpu_rollout.py), on a twin batch over the same steps of the same "
+                           "episodes as `value`; per-step obs / reward / done written; L2 flushed between "
+                           "launches"}
         del ro_obs, ro_out
 
     # episode statistics: the only cross-GPU reduction (sum + min), multigpu.reduce_stats
