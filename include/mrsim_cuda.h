@@ -294,8 +294,8 @@ int mrsim_step(mrsim_ctx* ctx, const int8_t* actions_dev, float* obs_dev, float*
  * rollout and the launch's drain is paid once. Outputs are step-major, each may be NULL:
  *   obs_dev [num_steps][num_envs][N][D] fp32, reward_dev [num_steps][num_envs] fp32,
  *   done_dev [num_steps][num_envs] uint8.
- * Requires the random policy (no feedforward / scripted policy), no trajectory capture and the
- * lane-group kernel (not MRSIM_FLAG_ENV_PER_THREAD): MRSIM_E_UNSUPPORTED otherwise.
+ * Requires MRSIM_FLAG_FP64, the random policy (no feedforward / scripted policy), no trajectory
+ * capture and the lane-group kernel (not MRSIM_FLAG_ENV_PER_THREAD): MRSIM_E_UNSUPPORTED otherwise.
  * Errors as mrsim_step (sticky, reported by mrsim_sync); a failing rollout is rolled back
  * as a whole, episode statistics included. */
 int mrsim_rollout(mrsim_ctx* ctx, int num_steps, float* obs_dev, float* reward_dev, uint8_t* done_dev,

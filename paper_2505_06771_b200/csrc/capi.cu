@@ -1007,9 +1007,9 @@ int mrsim_rollout(mrsim_ctx* ctx, int num_steps, float* obs_dev, float* reward_d
     if (!ctx->reset_done) return set_err(ctx, MRSIM_E_INVALID_ARGUMENT, "step before reset");
     if ((ctx->flags & MRSIM_FLAG_AUTO_RESET) && !ctx->has_episodes)
         return set_err(ctx, MRSIM_E_INVALID_ARGUMENT, "auto-reset needs mrsim_reset_episodes (episode seeds)");
-    if (ctx->ff || ctx->scripted || ctx->d_cap || ctx->L == 1)
+    if (ctx->ff || ctx->scripted || ctx->d_cap || ctx->L == 1 || !ctx->fp64)
         return set_err(ctx, MRSIM_E_UNSUPPORTED,
-                       "rollout: the harness random policy on the lane-group kernel only, without capture");
+                       "rollout: fp64, the harness random policy on the lane-group kernel, without capture");
     CK(cudaSetDevice(ctx->device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cudaError_t e;

@@ -3,13 +3,20 @@
 // precisions, and the reset kernel.
 #pragma once
 
+#include <type_traits>
+
 #include "launch.h"
 
 namespace mrsim_host {
 
 template <class Real, int L, int MP, int MO>
 static cudaError_t launch_V(const mrsim_dev::StepParams<Real>& p, int grid, int block, int smem, cudaStream_t stream) {
-    auto k = mrsim_dev::step_kernel<Real, L, MP, MO, MRSIM_TASK_ID>;
+    auto k = mrsim_dev::step_kernel<Real, L, MP, MO, MRSIM_TASK_ID, false>;
+    if constexpr (std::is_same_v<Real, double>) {  // mrsim_rollout (fp64 product path only)
+        if (p.n_steps > 1) k = mrsim_dev::step_kernel<Real, L, MP, MO, MRSIM_TASK_ID, true>;
+    } else {
+        if (p.n_steps > 1) return cudaErrorNotSupported;
+    }
     if (smem > 46 * 1024) {  // opt in above the 48 KB default, leaving room for the static tables
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;

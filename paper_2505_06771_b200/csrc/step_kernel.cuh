@@ -570,7 +570,9 @@ __host__ __device__ constexpr bool qp_fast_first_row(int L) {
     return L == 4;
 }
 
-template <class Real, int L, int MP, int MO, int TASK>
+// MULTI: the mrsim_rollout instantiation (p.n_steps steps per task); the single-step instantiation
+// compiles the step loop away (the loop and the input-copy select cost 2-6 % when always present).
+template <class Real, int L, int MP, int MO, int TASK, bool MULTI = false>
 __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(const __grid_constant__ StepParams<Real> p) {
     constexpr int G = 32 / L;  // envs per warp
     // Dynamic warp tasks: a warp takes the next G consecutive envs from a counter. Step k
@@ -625,8 +627,9 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
         // mrsim_rollout: n_steps consecutive steps of the task's envs in this launch. Step 0 reads
         // the input copy, later steps update the output copy in place (each env belongs to this
         // group alone), so the input copy stays untouched for the rollback of a failing launch.
-        for (int s = 0; s < p.n_steps; ++s) {
-            const DevState<Real>& in = (s == 0) ? p.in : p.out;
+        const int n_steps = MULTI ? p.n_steps : 1;
+        for (int s = 0; s < n_steps; ++s) {
+            const DevState<Real>& in = (MULTI && s > 0) ? p.out : p.in;
             float* const obs_s = p.obs ? p.obs + s * p.obs_step_stride : nullptr;
             float* const reward_s = p.reward ? p.reward + s * p.B : nullptr;
             uint8_t* const done_s = p.done ? p.done + s * p.B : nullptr;
