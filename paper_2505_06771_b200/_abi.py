@@ -101,8 +101,8 @@ FUNCTIONS = {
                                             c_void_p, c_void_p]),
     "mrsim_step": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "mrsim_rollout": (ctypes.c_int, [c_void_p, ctypes.c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
-    "mrsim_step_host": (ctypes.c_int, [c_void_p, P(ctypes.c_int32), P(ctypes.c_float), P(ctypes.c_double),
-                                       P(ctypes.c_uint8), c_void_p]),
+    # raw addresses (the host path is the e2e hot call: no per-call ctypes pointer objects)
+    "mrsim_step_host": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "mrsim_observe": (ctypes.c_int, [c_void_p, c_void_p, c_void_p]),
     "mrsim_observe_host": (ctypes.c_int, [c_void_p, P(ctypes.c_float)]),
     "mrsim_random_actions": (ctypes.c_int, [c_void_p, c_void_p, c_void_p]),

@@ -242,17 +242,23 @@ class CudaEnvBatch:
         """Synchronous step with host buffers (the reference's std::vector<int> actions).
         `out` = (obs float32 [B,N,D], reward float64 [B], done uint8 [B]) reuses caller
         buffers (pinned ones make the copies run at full link speed)."""
-        a = np.ascontiguousarray(np.asarray(actions, dtype=np.int32).reshape(self.num_envs, self.N))
+        a = actions
+        if not (isinstance(a, np.ndarray) and a.dtype == np.int32 and a.flags.c_contiguous and
+                a.size == self.num_envs * self.N):
+            a = np.ascontiguousarray(np.asarray(actions, dtype=np.int32).reshape(self.num_envs, self.N))
         if out is None:
             obs = np.empty((self.num_envs, self.N, self.D), dtype=np.float32)
             rew = np.empty((self.num_envs,), dtype=np.float64)
             done = np.empty((self.num_envs,), dtype=np.uint8)
+            ptrs = (obs.ctypes.data, rew.ctypes.data, done.ctypes.data)
         else:
             obs, rew, done = out
-        self._check(lib().mrsim_step_host(
-            self._h, a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
-            obs.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), rew.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
-            done.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), _stream_handle(None)))
+            key = (id(obs), id(rew), id(done))
+            cached = getattr(self, "_out_ptrs", None)
+            if cached is None or cached[0] != key:  # the caller's reused buffers: addresses looked up once
+                self._out_ptrs = (key, (obs.ctypes.data, rew.ctypes.data, done.ctypes.data), out)
+            ptrs = self._out_ptrs[1]
+        self._check(lib().mrsim_step_host(self._h, a.ctypes.data, ptrs[0], ptrs[1], ptrs[2], None))
         return obs, rew, done
 
     def observe(self):
