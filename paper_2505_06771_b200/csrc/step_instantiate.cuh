@@ -12,14 +12,22 @@ namespace mrsim_host {
 template <class Real, int L, int MP, int MO>
 static cudaError_t launch_V(const mrsim_dev::StepParams<Real>& p, int grid, int block, int smem, cudaStream_t stream) {
     auto k = mrsim_dev::step_kernel<Real, L, MP, MO, MRSIM_TASK_ID, false>;
+    static int opted[2][16] = {};  // dynamic shared memory already opted in, per instantiation and device
+    int multi = 0;
     if constexpr (std::is_same_v<Real, double>) {  // mrsim_rollout (fp64 product path only)
-        if (p.n_steps > 1) k = mrsim_dev::step_kernel<Real, L, MP, MO, MRSIM_TASK_ID, true>;
+        if (p.n_steps > 1) {
+            k = mrsim_dev::step_kernel<Real, L, MP, MO, MRSIM_TASK_ID, true>;
+            multi = 1;
+        }
     } else {
         if (p.n_steps > 1) return cudaErrorNotSupported;
     }
-    if (smem > 46 * 1024) {  // opt in above the 48 KB default, leaving room for the static tables
+    int dev = 0;
+    if (smem > 46 * 1024 && cudaGetDevice(&dev) == cudaSuccess && (dev >= 16 || smem > opted[multi][dev])) {
+        // opt in above the 48 KB default (static tables aside), once per device
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
+        if (dev < 16) opted[multi][dev] = smem;
     }
     k<<<grid, block, smem, stream>>>(p);
     return cudaGetLastError();

@@ -26,7 +26,7 @@ def _cfg(task, n):
                                     ("arctic_transport", 10), ("predator_prey", 6)])
 def test_rollout_equals_single_steps(task, n):
     cfg = _cfg(task, n)
-    B, T = 3000, 60  # crosses two auto-resets
+    B, T = 3001, 60  # crosses two auto-resets; a partial last warp task
     a = m.CudaEnvBatch(cfg, B, fp64=True, auto_reset=True)
     b = m.CudaEnvBatch(cfg, B, fp64=True, auto_reset=True)
     a.reset_episodes(root_seed=4)
@@ -52,7 +52,7 @@ def test_rollout_equals_single_steps(task, n):
 
 def test_rollout_in_chunks_and_mixed_with_steps():
     cfg = _cfg("navigation", 4)
-    B = 1000
+    B = 1003  # a partial last warp task (ghost groups)
     a = m.CudaEnvBatch(cfg, B, fp64=True, auto_reset=True)
     b = m.CudaEnvBatch(cfg, B, fp64=True, auto_reset=True)
     a.reset_episodes(root_seed=9)
