@@ -225,14 +225,25 @@ cudaError_t launch_scripted<double, MRSIM_TASK_ID>(const mrsim_dev::ScriptedPara
 
 }  // namespace mrsim_host
 
-#ifdef MRSIM_QP_STATS  // diagnostic builds only: the QP counters of this task's kernels
 #define MRSIM_DBG_CAT2(a, b) a##b
 #define MRSIM_DBG_CAT(a, b) MRSIM_DBG_CAT2(a, b)
+#ifdef MRSIM_QP_STATS  // diagnostic builds only: the QP counters of this task's kernels
 extern "C" int MRSIM_DBG_CAT(mrsim_debug_qp_stats_task, MRSIM_TASK_ID)(unsigned long long* out8, int reset) {
     if (cudaMemcpyFromSymbol(out8, mrsim_dev::g_qp_stats, 64) != cudaSuccess) return 1;
     if (reset) {
         unsigned long long z[8] = {0};
         cudaMemcpyToSymbol(mrsim_dev::g_qp_stats, z, 64);
+    }
+    return 0;
+}
+#endif
+
+#ifdef MRSIM_TASK_STATS  // diagnostic builds only: the warp-task duration histogram of this task's kernels
+extern "C" int MRSIM_DBG_CAT(mrsim_debug_task_hist_task, MRSIM_TASK_ID)(unsigned long long* out64, int reset) {
+    if (cudaMemcpyFromSymbol(out64, mrsim_dev::g_task_hist, 512) != cudaSuccess) return 1;
+    if (reset) {
+        unsigned long long z[64] = {0};
+        cudaMemcpyToSymbol(mrsim_dev::g_task_hist, z, 512);
     }
     return 0;
 }

@@ -522,6 +522,10 @@ __device__ __forceinline__ Real wrap_angle_dev(Real t) {
     return r;
 }
 
+#ifdef MRSIM_TASK_STATS
+__device__ unsigned long long g_task_hist[64];
+#endif
+
 template <class Real>
 struct Real2 {
     Real a, b;
@@ -624,6 +628,9 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
         const long long e_real = e0 + (gib & (G - 1));
         const bool ghost = e_real >= p.e_end;
         const long long e = ghost ? p.e_end - 1 : e_real;
+#ifdef MRSIM_TASK_STATS
+        const long long t_task0 = clock64();
+#endif
         // mrsim_rollout: n_steps consecutive steps of the task's envs in this launch. Step 0 reads
         // the input copy, later steps update the output copy in place (each env belongs to this
         // group alone), so the input copy stays untouched for the rollback of a failing launch.
@@ -938,6 +945,14 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
             }
             Grp<L>::sync();
         }  // rollout steps
+#ifdef MRSIM_TASK_STATS  // diagnostic builds: histogram of warp-task durations (log2 of SM cycles)
+        if ((threadIdx.x & 31) == 0) {
+            const long long dt = clock64() - t_task0;
+            const int b = dt > 0 ? 63 - __clzll(dt) : 0;
+            atomicAdd(&g_task_hist[b < 47 ? b : 47], 1ull);
+            atomicAdd(&g_task_hist[48], static_cast<unsigned long long>(dt));
+        }
+#endif
     }
 }
 
