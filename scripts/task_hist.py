@@ -11,6 +11,8 @@ task, n, B, steps, T = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), int(sys.
 cfg = m.make_default_config(task)
 if n != cfg.raw.num_robots:
     cfg.set_num_robots(n, tile_roster=cfg.raw.het_rows > 0)
+if task == "arctic_transport" and n > 4:
+    cfg.set_layout("arctic.spawn_zone", [-1.55, -1.05, -0.9, 0.9])  # bench.py ARCTIC_SPAWN
 cfg.max_steps = T
 gb = m.CudaEnvBatch(cfg, B, auto_reset=True)
 gb.reset_episodes(0)
