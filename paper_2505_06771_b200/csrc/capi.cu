@@ -50,6 +50,7 @@ struct mrsim_ctx {
     long long episode_stride = 0;
     long long env_steps = 0;
     std::string last_error;
+    std::vector<std::pair<char*, size_t>> guard_tails;  // checks builds: allocation guard tails
     int num_sms = 148;
     int block = 128;
     int grid = 0;
@@ -108,45 +109,103 @@ int cuda_fail(mrsim_ctx* ctx, cudaError_t e, const char* where) {
         if (_e != cudaSuccess) return cuda_fail(ctx, _e, #expr);    \
     } while (0)
 
+// SoA state copy layout: the fields in carve order, each 256-byte aligned (plus a guard gap
+// behind every field in -DMRSIM_DEVICE_CHECKS builds, verified by mrsim_debug_check_guards).
+#ifdef MRSIM_DEVICE_CHECKS
+constexpr size_t kStateGuard = 256;
+constexpr size_t kAllocGuard = 256;
+#else
+constexpr size_t kStateGuard = 0;
+constexpr size_t kAllocGuard = 0;
+#endif
+constexpr int kStateFields = 16;
+
+template <class Real>
+void state_field_bytes(long long B, int N, int nf, int ni, size_t (&f)[kStateFields]) {
+    const size_t R = sizeof(Real);
+    const size_t v[kStateFields] = {R * B * N, R * B * N, R * B * N,            // px, py, pt
+                                    4 * size_t(B),                              // step_index
+                                    8 * size_t(B), 8 * size_t(B), 8 * size_t(B),  // key, seed, pkey
+                                    8 * size_t(B),                              // episode
+                                    4 * size_t(B), 4 * size_t(B), 4 * size_t(B),  // collisions, qp_inf, success
+                                    R * B, R * B, R * B,                        // metric, min_dist, ep_return
+                                    R * B * (nf > 0 ? nf : 1), 4 * size_t(B) * (ni > 0 ? ni : 1)};  // tf, ti
+    for (int k = 0; k < kStateFields; ++k) f[k] = v[k];
+}
+inline size_t state_slot(size_t bytes) { return ((bytes + 255) & ~size_t(255)) + kStateGuard; }
+
 template <class Real>
 size_t state_bytes(long long B, int N, int nf, int ni) {
-    size_t b = 0;
-    auto add = [&](size_t bytes) { b += (bytes + 255) & ~size_t(255); };
-    for (int k = 0; k < 3; ++k) add(sizeof(Real) * B * N);
-    add(4 * B);                      // step_index
-    for (int k = 0; k < 3; ++k) add(8 * B);  // key, seed, pkey
-    add(8 * B);                      // episode
-    for (int k = 0; k < 3; ++k) add(4 * B);  // collisions, qp_inf, success
-    for (int k = 0; k < 3; ++k) add(sizeof(Real) * B);  // metric, min_dist, ep_return
-    add(sizeof(Real) * B * (nf > 0 ? nf : 1));
-    add(4 * B * (ni > 0 ? ni : 1));
+    size_t f[kStateFields], b = 0;
+    state_field_bytes<Real>(B, N, nf, ni, f);
+    for (size_t x : f) b += state_slot(x);
     return b;
 }
 
 template <class Real>
 void carve_state(void* base, long long B, int N, int nf, int ni, DevState<Real>& s) {
+    size_t f[kStateFields];
+    state_field_bytes<Real>(B, N, nf, ni, f);
     char* p = static_cast<char*>(base);
-    auto take = [&](size_t bytes) {
-        char* r = p;
-        p += (bytes + 255) & ~size_t(255);
-        return r;
-    };
-    s.px = reinterpret_cast<Real*>(take(sizeof(Real) * B * N));
-    s.py = reinterpret_cast<Real*>(take(sizeof(Real) * B * N));
-    s.pt = reinterpret_cast<Real*>(take(sizeof(Real) * B * N));
-    s.step_index = reinterpret_cast<int32_t*>(take(4 * B));
-    s.key = reinterpret_cast<uint64_t*>(take(8 * B));
-    s.seed = reinterpret_cast<uint64_t*>(take(8 * B));
-    s.pkey = reinterpret_cast<uint64_t*>(take(8 * B));
-    s.episode = reinterpret_cast<int64_t*>(take(8 * B));
-    s.collisions = reinterpret_cast<int32_t*>(take(4 * B));
-    s.qp_inf = reinterpret_cast<int32_t*>(take(4 * B));
-    s.success = reinterpret_cast<int32_t*>(take(4 * B));
-    s.metric = reinterpret_cast<Real*>(take(sizeof(Real) * B));
-    s.min_dist = reinterpret_cast<Real*>(take(sizeof(Real) * B));
-    s.ep_return = reinterpret_cast<Real*>(take(sizeof(Real) * B));
-    s.tf = reinterpret_cast<Real*>(take(sizeof(Real) * B * (nf > 0 ? nf : 1)));
-    s.ti = reinterpret_cast<int32_t*>(take(4 * B * (ni > 0 ? ni : 1)));
+    char* at[kStateFields];
+    for (int k = 0; k < kStateFields; ++k) {
+        at[k] = p;
+        p += state_slot(f[k]);
+    }
+    s.px = reinterpret_cast<Real*>(at[0]);
+    s.py = reinterpret_cast<Real*>(at[1]);
+    s.pt = reinterpret_cast<Real*>(at[2]);
+    s.step_index = reinterpret_cast<int32_t*>(at[3]);
+    s.key = reinterpret_cast<uint64_t*>(at[4]);
+    s.seed = reinterpret_cast<uint64_t*>(at[5]);
+    s.pkey = reinterpret_cast<uint64_t*>(at[6]);
+    s.episode = reinterpret_cast<int64_t*>(at[7]);
+    s.collisions = reinterpret_cast<int32_t*>(at[8]);
+    s.qp_inf = reinterpret_cast<int32_t*>(at[9]);
+    s.success = reinterpret_cast<int32_t*>(at[10]);
+    s.metric = reinterpret_cast<Real*>(at[11]);
+    s.min_dist = reinterpret_cast<Real*>(at[12]);
+    s.ep_return = reinterpret_cast<Real*>(at[13]);
+    s.tf = reinterpret_cast<Real*>(at[14]);
+    s.ti = reinterpret_cast<int32_t*>(at[15]);
+}
+
+// Guard regions of a state copy at `base`: [offset, offset + kStateGuard) behind every field.
+template <class Real>
+void state_guards(long long B, int N, int nf, int ni, std::vector<size_t>& offsets) {
+    size_t f[kStateFields], b = 0;
+    state_field_bytes<Real>(B, N, nf, ni, f);
+    for (size_t x : f) {
+        b += state_slot(x);
+        offsets.push_back(b - kStateGuard);
+    }
+}
+
+// Device allocation owned by the context: in checks builds with a guard tail of kAllocGuard
+// pattern bytes, registered for mrsim_debug_check_guards.
+template <class T>
+cudaError_t ctx_malloc(mrsim_ctx* ctx, T** ptr, size_t bytes) {
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(ptr), bytes + kAllocGuard);
+    if (e != cudaSuccess || !kAllocGuard) return e;
+    e = cudaMemset(reinterpret_cast<char*>(*ptr) + bytes, 0xA5, kAllocGuard);
+    ctx->guard_tails.emplace_back(reinterpret_cast<char*>(*ptr) + bytes, kAllocGuard);
+    return e;
+}
+// cudaFree of a ctx_malloc allocation, dropping its guard tail: the registered tail nearest
+// above the allocation's start (allocations do not overlap).
+template <class T>
+void ctx_free(mrsim_ctx* ctx, T* ptr) {
+    if (!ptr) return;
+    if (kAllocGuard) {
+        char* const lo = reinterpret_cast<char*>(ptr);
+        size_t best = ctx->guard_tails.size();
+        for (size_t i = 0; i < ctx->guard_tails.size(); ++i)
+            if (ctx->guard_tails[i].first >= lo &&
+                (best == ctx->guard_tails.size() || ctx->guard_tails[i].first < ctx->guard_tails[best].first))
+                best = i;
+        if (best < ctx->guard_tails.size()) ctx->guard_tails.erase(ctx->guard_tails.begin() + best);
+    }
+    cudaFree(ptr);
 }
 
 // ---- dispatch tables over the task template parameter ----
@@ -488,6 +547,11 @@ cudaError_t host_mirror(mrsim_ctx* ctx, DevState<Real>& h) {
             ctx->h_state = nullptr;
             return e;
         }
+        if (kStateGuard) {  // whole-block uploads carry the mirror's guard gaps to the device copy
+            std::vector<size_t> gaps;
+            state_guards<Real>(ctx->B, ctx->N, ctx->nf, ctx->ni, gaps);
+            for (size_t off : gaps) std::memset(static_cast<char*>(ctx->h_state) + off, 0xA5, kStateGuard);
+        }
     }
     carve_state(ctx->h_state, ctx->B, ctx->N, ctx->nf, ctx->ni, h);
     return cudaSuccess;
@@ -763,10 +827,10 @@ int capture_step(mrsim_ctx* ctx, const int8_t* actions, float* obs, float* rewar
     if (ctx->cap_steps >= ctx->cap_max) return set_err(ctx, MRSIM_E_INVALID_ARGUMENT, "trajectory capture buffer full");
     CK(cudaSetDevice(ctx->device));
     const long long BN = ctx->B * ctx->N;
-    if (!ctx->d_reward64) CK(cudaMalloc(&ctx->d_reward64, 8 * ctx->B));
-    if (!ctx->d_done) CK(cudaMalloc(&ctx->d_done, ctx->B));
+    if (!ctx->d_reward64) CK(ctx_malloc(ctx, &ctx->d_reward64, 8 * ctx->B));
+    if (!ctx->d_done) CK(ctx_malloc(ctx, &ctx->d_done, ctx->B));
     if (!actions) {
-        if (!ctx->d_pol_actions) CK(cudaMalloc(&ctx->d_pol_actions, BN));
+        if (!ctx->d_pol_actions) CK(ctx_malloc(ctx, &ctx->d_pol_actions, BN));
         const bool dev_policy = ctx->ff || ctx->scripted;
         int rc = dev_policy ? run_policy(ctx, ctx->d_pol_actions, s) : MRSIM_OK;
         if (!dev_policy) {
@@ -836,15 +900,21 @@ int mrsim_create(const mrsim_cfg* cfg, int device, int64_t num_envs, uint32_t fl
     const size_t sb = ctx->fp64 ? state_bytes<double>(ctx->B, ctx->N, ctx->nf, ctx->ni)
                                 : state_bytes<float>(ctx->B, ctx->N, ctx->nf, ctx->ni);
     for (int k = 0; k < 2; ++k) {
-        if ((e = cudaMalloc(&ctx->mem[k], sb)) != cudaSuccess) return bail(e, "cudaMalloc state");
+        if ((e = ctx_malloc(ctx, &ctx->mem[k], sb)) != cudaSuccess) return bail(e, "cudaMalloc state");
         cudaMemset(ctx->mem[k], 0, sb);
+        if (kStateGuard) {
+            std::vector<size_t> gaps;
+            if (ctx->fp64) state_guards<double>(ctx->B, ctx->N, ctx->nf, ctx->ni, gaps);
+            else state_guards<float>(ctx->B, ctx->N, ctx->nf, ctx->ni, gaps);
+            for (size_t off : gaps) cudaMemset(static_cast<char*>(ctx->mem[k]) + off, 0xA5, kStateGuard);
+        }
         if (ctx->fp64) carve_state(ctx->mem[k], ctx->B, ctx->N, ctx->nf, ctx->ni, ctx->sd[k]);
         else carve_state(ctx->mem[k], ctx->B, ctx->N, ctx->nf, ctx->ni, ctx->sf[k]);
     }
     // stats + undo log (values before the last update) + update serial; 256-byte aligned arrays
     const size_t stb = 2 * (static_cast<size_t>(ctx->B) * (4 + 8 * 5 + 8 * 2) + 8 * 256) +
                        static_cast<size_t>(ctx->B) * 8 + 256;
-    if ((e = cudaMalloc(&ctx->stats_mem, stb)) != cudaSuccess) return bail(e, "cudaMalloc stats");
+    if ((e = ctx_malloc(ctx, &ctx->stats_mem, stb)) != cudaSuccess) return bail(e, "cudaMalloc stats");
     {
         char* p = static_cast<char*>(ctx->stats_mem);
         auto take = [&](size_t bytes) {
@@ -876,7 +946,7 @@ int mrsim_create(const mrsim_cfg* cfg, int device, int64_t num_envs, uint32_t fl
         cudaMemcpy(st.min_dist, inf.data(), 8 * ctx->B, cudaMemcpyHostToDevice);
     }
     // error word, its step serial, then the step kernel's two warp-task counters
-    if ((e = cudaMalloc(&ctx->d_err, 32)) != cudaSuccess) return bail(e, "cudaMalloc err");
+    if ((e = ctx_malloc(ctx, &ctx->d_err, 32)) != cudaSuccess) return bail(e, "cudaMalloc err");
     ctx->d_err_serial = reinterpret_cast<long long*>(ctx->d_err + 1);
     ctx->d_ticket = reinterpret_cast<unsigned*>(ctx->d_err + 2);  // step kernel [2], scripted kernel [2]
     cudaMemset(ctx->d_ticket, 0, 16);
@@ -928,9 +998,19 @@ int mrsim_create(const mrsim_cfg* cfg, int device, int64_t num_envs, uint32_t fl
     return MRSIM_OK;
 }
 
+#ifdef MRSIM_DEVICE_CHECKS
+int mrsim_debug_check_guards(mrsim_ctx* ctx);
+#endif
+
 void mrsim_destroy(mrsim_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
+#ifdef MRSIM_DEVICE_CHECKS
+    if (mrsim_debug_check_guards(ctx) == MRSIM_E_RUNTIME) {  // a guard was overwritten: fail the whole run
+        std::fprintf(stderr, "MRSIM_DEVICE_CHECKS: %s\n", ctx->last_error.c_str());
+        std::abort();
+    }
+#endif
     for (int k = 0; k < 2; ++k) cudaFree(ctx->mem[k]);
     cudaFree(ctx->stats_mem);
     cudaFree(ctx->d_err);
@@ -940,10 +1020,10 @@ void mrsim_destroy(mrsim_ctx* ctx) {
     cudaFree(ctx->d_done);
     if (ctx->h_err) cudaFreeHost(ctx->h_err);
     if (ctx->h_state) cudaFreeHost(ctx->h_state);
-    cudaFree(ctx->d_wT);
-    cudaFree(ctx->d_bias);
+    ctx_free(ctx, ctx->d_wT);
+    ctx_free(ctx, ctx->d_bias);
     cudaFree(ctx->d_pol_actions);
-    cudaFree(ctx->d_cap);
+    ctx_free(ctx, ctx->d_cap);
     delete ctx;
 }
 
@@ -1055,20 +1135,20 @@ int mrsim_step_host(mrsim_ctx* ctx, const int32_t* actions_host, float* obs_host
     double* rew = mapped_alias(reward_host);
     uint8_t* done = mapped_alias(done_host);
     if (!act) {
-        if (!ctx->d_actions32) CK(cudaMalloc(&ctx->d_actions32, 4 * BN));
+        if (!ctx->d_actions32) CK(ctx_malloc(ctx, &ctx->d_actions32, 4 * BN));
         CK(cudaMemcpyAsync(ctx->d_actions32, actions_host, 4 * BN, cudaMemcpyHostToDevice, s));
         act = ctx->d_actions32;
     }
     if (obs_host && !obs) {
-        if (!ctx->d_obs) CK(cudaMalloc(&ctx->d_obs, obs_bytes));
+        if (!ctx->d_obs) CK(ctx_malloc(ctx, &ctx->d_obs, obs_bytes));
         obs = ctx->d_obs;
     }
     if (reward_host && !rew) {
-        if (!ctx->d_reward64) CK(cudaMalloc(&ctx->d_reward64, 8 * ctx->B));
+        if (!ctx->d_reward64) CK(ctx_malloc(ctx, &ctx->d_reward64, 8 * ctx->B));
         rew = ctx->d_reward64;
     }
     if (done_host && !done) {
-        if (!ctx->d_done) CK(cudaMalloc(&ctx->d_done, ctx->B));
+        if (!ctx->d_done) CK(ctx_malloc(ctx, &ctx->d_done, ctx->B));
         done = ctx->d_done;
     }
     // The reference's std::vector<int> goes up as is; validate_actions (batch.hpp:226-237) runs in the
@@ -1103,7 +1183,7 @@ int mrsim_observe_host(mrsim_ctx* ctx, float* obs_host) {
     if (!ctx || !obs_host) return MRSIM_E_INVALID_ARGUMENT;
     CK(cudaSetDevice(ctx->device));
     const size_t obs_bytes = sizeof(float) * ctx->B * ctx->N * ctx->D;
-    if (!ctx->d_obs) CK(cudaMalloc(&ctx->d_obs, obs_bytes));
+    if (!ctx->d_obs) CK(ctx_malloc(ctx, &ctx->d_obs, obs_bytes));
     int rc = mrsim_observe(ctx, ctx->d_obs, nullptr);
     if (rc != MRSIM_OK) return rc;
     CK(cudaMemcpy(obs_host, ctx->d_obs, obs_bytes, cudaMemcpyDeviceToHost));
@@ -1129,7 +1209,7 @@ int mrsim_set_policy_scripted(mrsim_ctx* ctx, int kind) {
     if (cols * rows > mrsim_dev::kGridMaxCells)
         return set_err(ctx, MRSIM_E_UNSUPPORTED, "scripted planner grid exceeds the device capacity");
     CK(cudaSetDevice(ctx->device));
-    if (!ctx->d_pol_actions) CK(cudaMalloc(&ctx->d_pol_actions, ctx->B * ctx->N));
+    if (!ctx->d_pol_actions) CK(ctx_malloc(ctx, &ctx->d_pol_actions, ctx->B * ctx->N));
     ctx->ff = false;
     ctx->scripted = kind;
     return MRSIM_OK;
@@ -1180,16 +1260,16 @@ int mrsim_set_policy_feedforward(mrsim_ctx* ctx, int num_layers, const int32_t* 
     }
     CK(cudaSetDevice(ctx->device));
     CK(cudaDeviceSynchronize());
-    cudaFree(ctx->d_wT);
-    cudaFree(ctx->d_bias);
+    ctx_free(ctx, ctx->d_wT);
+    ctx_free(ctx, ctx->d_bias);
     ctx->d_wT = nullptr;
     ctx->d_bias = nullptr;
     ctx->ff = false;
-    CK(cudaMalloc(&ctx->d_wT, sizeof(double) * wT.size()));
-    CK(cudaMalloc(&ctx->d_bias, sizeof(double) * bias.size()));
+    CK(ctx_malloc(ctx, &ctx->d_wT, sizeof(double) * wT.size()));
+    CK(ctx_malloc(ctx, &ctx->d_bias, sizeof(double) * bias.size()));
     CK(cudaMemcpy(ctx->d_wT, wT.data(), sizeof(double) * wT.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->d_bias, bias.data(), sizeof(double) * bias.size(), cudaMemcpyHostToDevice));
-    if (!ctx->d_pol_actions) CK(cudaMalloc(&ctx->d_pol_actions, ctx->B * ctx->N));
+    if (!ctx->d_pol_actions) CK(ctx_malloc(ctx, &ctx->d_pol_actions, ctx->B * ctx->N));
     ctx->net = net;
     ctx->ff = true;
     ctx->scripted = 0;
@@ -1226,10 +1306,10 @@ int mrsim_capture_begin(mrsim_ctx* ctx, int64_t max_steps) {
         return set_err(ctx, MRSIM_E_INVALID_ARGUMENT, "trajectory capture needs a context without auto-reset");
     CK(cudaSetDevice(ctx->device));
     CK(cudaDeviceSynchronize());
-    cudaFree(ctx->d_cap);
+    ctx_free(ctx, ctx->d_cap);
     ctx->d_cap = nullptr;
     ctx->cap_max = ctx->cap_steps = 0;
-    CK(cudaMalloc(&ctx->d_cap, sizeof(mrsim_traj_record) * max_steps * ctx->B * ctx->N));
+    CK(ctx_malloc(ctx, &ctx->d_cap, sizeof(mrsim_traj_record) * max_steps * ctx->B * ctx->N));
     ctx->cap_max = max_steps;
     return MRSIM_OK;
 }
@@ -1252,7 +1332,7 @@ int mrsim_capture_end(mrsim_ctx* ctx) {
     if (!ctx) return MRSIM_E_INVALID_ARGUMENT;
     CK(cudaSetDevice(ctx->device));
     CK(cudaDeviceSynchronize());
-    cudaFree(ctx->d_cap);
+    ctx_free(ctx, ctx->d_cap);
     ctx->d_cap = nullptr;
     ctx->cap_max = ctx->cap_steps = 0;
     return MRSIM_OK;
@@ -1316,5 +1396,48 @@ int mrsim_get_stats(mrsim_ctx* ctx, mrsim_stats* out) {
     *out = s;
     return MRSIM_OK;
 }
+
+#ifdef MRSIM_DEVICE_CHECKS
+// Checks builds only: verify every guard gap of both state copies and every allocation's guard
+// tail still holds the fill pattern (an out-of-bounds device write lands in one of them).
+int mrsim_debug_check_guards(mrsim_ctx* ctx) {
+    if (!ctx) return MRSIM_E_INVALID_ARGUMENT;
+    CK(cudaDeviceSynchronize());
+    std::vector<unsigned char> buf(kStateGuard > kAllocGuard ? kStateGuard : kAllocGuard);
+    auto bad = [&](size_t n) {
+        for (size_t i = 0; i < n; ++i)
+            if (buf[i] != 0xA5) return true;
+        return false;
+    };
+    std::vector<size_t> gaps;
+    if (ctx->fp64) state_guards<double>(ctx->B, ctx->N, ctx->nf, ctx->ni, gaps);
+    else state_guards<float>(ctx->B, ctx->N, ctx->nf, ctx->ni, gaps);
+    for (int k = 0; k < 2; ++k)
+        for (size_t f = 0; f < gaps.size(); ++f) {
+            CK(cudaMemcpy(buf.data(), static_cast<char*>(ctx->mem[k]) + gaps[f], kStateGuard, cudaMemcpyDeviceToHost));
+            if (bad(kStateGuard))
+                return set_err(ctx, MRSIM_E_RUNTIME, "guard overwritten: state copy " + std::to_string(k) +
+                                                          " behind field " + std::to_string(f));
+        }
+    for (size_t t = 0; t < ctx->guard_tails.size(); ++t) {
+        CK(cudaMemcpy(buf.data(), ctx->guard_tails[t].first, kAllocGuard, cudaMemcpyDeviceToHost));
+        if (bad(kAllocGuard)) return set_err(ctx, MRSIM_E_RUNTIME, "guard overwritten: allocation tail " + std::to_string(t));
+    }
+    return MRSIM_OK;
+}
+
+// Checks builds only, negative control: overwrite the first byte of a guard (which = 0: the
+// state guard behind field 0 of copy 0; 1: the first allocation tail) with `value` (0xA5 restores).
+int mrsim_debug_poke_guard(mrsim_ctx* ctx, int which, int value) {
+    if (!ctx || which < 0 || which > 1 || (which == 1 && ctx->guard_tails.empty())) return MRSIM_E_INVALID_ARGUMENT;
+    std::vector<size_t> gaps;
+    if (ctx->fp64) state_guards<double>(ctx->B, ctx->N, ctx->nf, ctx->ni, gaps);
+    else state_guards<float>(ctx->B, ctx->N, ctx->nf, ctx->ni, gaps);
+    char* at = which == 0 ? static_cast<char*>(ctx->mem[0]) + gaps[0] : ctx->guard_tails[0].first;
+    CK(cudaMemset(at, value & 0xff, 1));
+    CK(cudaDeviceSynchronize());
+    return MRSIM_OK;
+}
+#endif
 
 }  // extern "C"

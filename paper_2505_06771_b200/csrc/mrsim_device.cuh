@@ -13,9 +13,33 @@
 #endif
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 #include "mrsim_cuda.h"
+
+// Device bounds checks (builds with -DMRSIM_DEVICE_CHECKS only; scripts/device_checks.sh): the
+// substitute for compute-sanitizer, which this GPU pool refuses. Index asserts at the shared
+// accessors, guard words between every shared-memory sub-array of a group (filled per task and
+// verified at its end) and guard tails behind the context's device allocations. A failed check
+// prints its site and traps, so the launch fails and every test using it fails loudly.
+#ifdef MRSIM_DEVICE_CHECKS
+#define MRSIM_DCHECK(cond)                                                                              \
+    do {                                                                                                \
+        if (!(cond)) {                                                                                  \
+            printf("MRSIM_DCHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond,  \
+                   static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));                        \
+            __trap();                                                                                   \
+        }                                                                                               \
+    } while (0)
+#define MRSIM_GUARD_WORDS 4  // 16-byte guard between shared sub-arrays
+#else
+#define MRSIM_DCHECK(cond) \
+    do {                   \
+    } while (0)
+#define MRSIM_GUARD_WORDS 0
+#endif
+constexpr unsigned kGuardPattern = 0xA5C3E10Fu;
 
 namespace mrsim_dev {
 

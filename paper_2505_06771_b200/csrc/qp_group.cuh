@@ -59,19 +59,46 @@ struct QpWs {
     Desc* desc;
     int* act;
     int* warm;  // the group's previous active rows, in logical order (warm-started entering order)
+    static constexpr int kGuardBytes = 4 * MRSIM_GUARD_WORDS;  // checks builds: a guard behind each array
     static __host__ __device__ constexpr int bytes(int n) {
-        return static_cast<int>(sizeof(Real)) * (n * n + 3 * n) + static_cast<int>(sizeof(Desc)) * n + 8 * n;
+        return static_cast<int>(sizeof(Real)) * (n * n + 3 * n) + static_cast<int>(sizeof(Desc)) * n + 8 * n +
+               7 * kGuardBytes;
     }
     __device__ void carve(unsigned char* base, int n) {
         S = reinterpret_cast<Real*>(base);
+#if MRSIM_GUARD_WORDS
+        lam = reinterpret_cast<Real*>(reinterpret_cast<unsigned char*>(S + n * n) + kGuardBytes);
+        r = reinterpret_cast<Real*>(reinterpret_cast<unsigned char*>(lam + n) + kGuardBytes);
+        d = reinterpret_cast<Real*>(reinterpret_cast<unsigned char*>(r + n) + kGuardBytes);
+        desc = reinterpret_cast<Desc*>(reinterpret_cast<unsigned char*>(d + n) + kGuardBytes);
+        act = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(desc + n) + kGuardBytes);
+        warm = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(act + n) + kGuardBytes);
+#else
         lam = S + n * n;
         r = lam + n;
         d = r + n;
         desc = reinterpret_cast<Desc*>(d + n);
         act = reinterpret_cast<int*>(desc + n);
         warm = act + n;
+#endif
     }
+#if MRSIM_GUARD_WORDS
+    // guard word g (0..7*4) of this workspace for n variables
+    __device__ unsigned* guard(int n, int k) const {
+        unsigned char* const ends[7] = {reinterpret_cast<unsigned char*>(S + n * n),
+                                        reinterpret_cast<unsigned char*>(lam + n),
+                                        reinterpret_cast<unsigned char*>(r + n),
+                                        reinterpret_cast<unsigned char*>(d + n),
+                                        reinterpret_cast<unsigned char*>(desc + n),
+                                        reinterpret_cast<unsigned char*>(act + n),
+                                        reinterpret_cast<unsigned char*>(warm + n)};
+        return reinterpret_cast<unsigned*>(ends[k / MRSIM_GUARD_WORDS]) + k % MRSIM_GUARD_WORDS;
+    }
+#endif
 };
+
+// Checked slot index of the QP workspace (checks builds; no-op otherwise).
+#define MRSIM_QP_SLOT_OK(q, n) MRSIM_DCHECK((q) >= 0 && (q) < (n))
 
 // Solve for the groups with `participate` set. (ux, uy): this lane's pair of
 // variables (in: u_nom, out: solution). Returns the QpStatusDev of the group.
@@ -109,6 +136,7 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
     const int max_iterations = 100 + 20 * total_rows;  // qp.hpp:193
     if constexpr (WARM) {
         const int wk = participate ? *warm_k : 0;  // previous active rows (group-uniform)
+        MRSIM_DCHECK(wk >= 0 && wk <= n);
         const int wmax = Grp<L>::warp_max(wk);
         if (wmax > 0) {
             const Real ux0 = ux, uy0 = uy;
@@ -294,6 +322,7 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
         }
         while (Grp<L>::warp_any(in)) {  // qp.hpp:262-330
             const bool s0 = in && lp0 >= 0, s1 = in && lp1 >= 0;  // own active slots
+            MRSIM_DCHECK((!s0 || q0 < n) && (!s1 || q1 < n) && (n >= 32 || (amask >> n) == 0u));
             // d = N^T g
             if (s0) ws.d[q0] = rows.dot(ws.desc[q0], gd);
             if (s1) ws.d[q1] = rows.dot(ws.desc[q1], gd);
@@ -388,6 +417,7 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
             if (do_add) {  // bordered inverse: the new slot's Schur complement is |z|^2
                 const Real is = Real(1) / z2;
                 const int qk = __ffs(~amask) - 1;  // lowest free physical slot
+                MRSIM_QP_SLOT_OK(qk, n);
                 if (s0) {
                     const Real ra = r0 * is;
                     for (unsigned m = amask; m; m &= m - 1) {
@@ -420,6 +450,7 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
                 ++k;
             }
             if (do_drop) {  // S <- S_{-b,-b} - S_{-b,b} S_{b,-b} / S_bb; later slots move up one logical place
+                MRSIM_DCHECK(qb < n && ((amask >> qb) & 1u));
                 rows.set_active(g, ws.act[qb], false);
                 const unsigned rest = amask & ~(1u << qb);
                 const Real ib = Real(1) / ws.S[qb * n + qb];

@@ -191,7 +191,10 @@ struct BarrierRows {
     unsigned active;
     bool valid;  // this lane carries a robot
 
-    __device__ __forceinline__ Real& F(int f, int lane) const { return rc[f * L + lane]; }
+    __device__ __forceinline__ Real& F(int f, int lane) const {
+        MRSIM_DCHECK(f >= 0 && f < kFields && lane >= 0 && lane < L);
+        return rc[f * L + lane];
+    }
     __device__ __forceinline__ int dummy_row() const { return off_box; }
 
     // A lane scans its rows in increasing global index, so the reference's
@@ -266,6 +269,7 @@ struct BarrierRows {
             ogy_b = F(f + 1, ow);
             oh_b = F(f + 2, ow);
         }
+        MRSIM_DCHECK(p >= 0 && p <= off_box + 4 * N);
         Desc dsc;
         if (p < P) {  // pair (i, j): -(gx, gy) on i, +(gx, gy) on j
             const int owner = p & (L - 1), s = p / L;
@@ -482,16 +486,35 @@ struct GroupSmem {
     QpWs<Real, BarrierDesc<Real>> qp;
     Real *xs, *ys, *ts, *tf, *rc;
     int *ti, *misc, *drones, *dcell;
+    static constexpr int kG = 4 * MRSIM_GUARD_WORDS;  // checks builds: a guard behind each array
+    static constexpr int kGuards = 9;
     static __host__ __device__ int rc_reals(int L, int MP, int MO) { return (3 * MP + 4 + 3 * MO + 2) * L; }
     static __host__ __device__ int bytes(int N, int nf, int ni, int L, int MP, int MO) {
         const int qb = (QpWs<Real, BarrierDesc<Real>>::bytes(2 * N) + 15) & ~15;
         const int reals = 3 * N + nf + rc_reals(L, MP, MO);
         const int ints = ni + 2 + N + 2 * N;  // task words, misc, drone list, drone cells
-        const int b = qb + reals * static_cast<int>(sizeof(Real)) + ints * 4;
+        const int b = qb + reals * static_cast<int>(sizeof(Real)) + ints * 4 + kGuards * kG;
         return (b + 15) & ~15;
     }
-    __device__ void carve(unsigned char* base, int N, int nf, int rcr) {
+    __device__ void carve(unsigned char* base, int N, int nf, int ni, int rcr) {
         qp.carve(base, 2 * N);
+#if MRSIM_GUARD_WORDS
+        unsigned char* b = base + ((QpWs<Real, BarrierDesc<Real>>::bytes(2 * N) + 15) & ~15);
+        auto take = [&](int bytes) {
+            unsigned char* r = b;
+            b += bytes + kG;
+            return r;
+        };
+        xs = reinterpret_cast<Real*>(take(N * static_cast<int>(sizeof(Real))));
+        ys = reinterpret_cast<Real*>(take(N * static_cast<int>(sizeof(Real))));
+        ts = reinterpret_cast<Real*>(take(N * static_cast<int>(sizeof(Real))));
+        tf = reinterpret_cast<Real*>(take(nf * static_cast<int>(sizeof(Real))));
+        rc = reinterpret_cast<Real*>(take(rcr * static_cast<int>(sizeof(Real))));
+        ti = reinterpret_cast<int*>(take(4 * ni));
+        misc = reinterpret_cast<int*>(take(4 * 2));
+        drones = reinterpret_cast<int*>(take(4 * N));
+        dcell = reinterpret_cast<int*>(take(4 * 2 * N));
+#else
         Real* r = reinterpret_cast<Real*>(base + ((QpWs<Real, BarrierDesc<Real>>::bytes(2 * N) + 15) & ~15));
         xs = r;
         ys = xs + N;
@@ -499,9 +522,35 @@ struct GroupSmem {
         tf = ts + N;
         rc = tf + nf;
         ti = reinterpret_cast<int*>(rc + rcr);
-        misc = ti;  // misc words follow the ni task words (set by the kernel)
-        drones = nullptr;
+        misc = ti + ni;
+        drones = misc + 2;
+        dcell = drones + N;
+#endif
     }
+#if MRSIM_GUARD_WORDS
+    // guard words behind each array (group lane 0 fills them per task and checks them at its end)
+    __device__ unsigned* guard(int k, int N, int nf, int ni, int rcr) const {
+        unsigned char* const ends[kGuards] = {
+            reinterpret_cast<unsigned char*>(xs + N),  reinterpret_cast<unsigned char*>(ys + N),
+            reinterpret_cast<unsigned char*>(ts + N),  reinterpret_cast<unsigned char*>(tf + nf),
+            reinterpret_cast<unsigned char*>(rc + rcr), reinterpret_cast<unsigned char*>(ti + ni),
+            reinterpret_cast<unsigned char*>(misc + 2), reinterpret_cast<unsigned char*>(drones + N),
+            reinterpret_cast<unsigned char*>(dcell + 2 * N)};
+        return reinterpret_cast<unsigned*>(ends[k / MRSIM_GUARD_WORDS]) + k % MRSIM_GUARD_WORDS;
+    }
+    __device__ void guards(bool fill, int N, int nf, int ni, int rcr) const {
+        for (int k = 0; k < kGuards * MRSIM_GUARD_WORDS; ++k) {
+            unsigned* w = guard(k, N, nf, ni, rcr);
+            if (fill) *w = kGuardPattern;
+            else MRSIM_DCHECK(*w == kGuardPattern);
+        }
+        for (int k = 0; k < 7 * MRSIM_GUARD_WORDS; ++k) {
+            unsigned* w = qp.guard(2 * N, k);
+            if (fill) *w = kGuardPattern;
+            else MRSIM_DCHECK(*w == kGuardPattern);
+        }
+    }
+#endif
 };
 
 // wrap_angle (core.hpp:102-108) for |t| < 3*pi: remainder(t, 2*pi) is t -/+ 2*pi,
@@ -593,10 +642,10 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
     const mrsim_cfg& c = p.c;
     const int N = p.N;
     GroupSmem<Real> sm;
-    sm.carve(smem_raw + gib * p.smem_bytes_per_group, N, p.nf, GroupSmem<Real>::rc_reals(L, MP, MO));
-    int* misc = sm.ti + p.ni;
-    sm.drones = misc + 2;
-    sm.dcell = sm.drones + N;
+    sm.carve(smem_raw + gib * p.smem_bytes_per_group, N, p.nf, p.ni, GroupSmem<Real>::rc_reals(L, MP, MO));
+    int* misc = sm.misc;
+    MRSIM_DCHECK(reinterpret_cast<unsigned char*>(sm.dcell + 2 * N) + GroupSmem<Real>::kG <=
+                 smem_raw + (gib + 1) * p.smem_bytes_per_group);
     int n_drones = 0;
     if (TASK == MRSIM_TASK_ARCTIC_TRANSPORT) n_drones = arctic_drones(c, sm.drones);
 
@@ -628,6 +677,11 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
         const long long e_real = e0 + (gib & (G - 1));
         const bool ghost = e_real >= p.e_end;
         const long long e = ghost ? p.e_end - 1 : e_real;
+        MRSIM_DCHECK(e >= 0 && e < p.B);
+#if MRSIM_GUARD_WORDS
+        if (lane == 0) sm.guards(true, N, p.nf, p.ni, GroupSmem<Real>::rc_reals(L, MP, MO));
+        Grp<L>::sync();
+#endif
 #ifdef MRSIM_TASK_STATS
         const long long t_task0 = clock64();
 #endif
@@ -865,6 +919,7 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
                 float* wst = reinterpret_cast<float*>(smem_raw + gpb * p.smem_bytes_per_group) +
                              (threadIdx.x >> 5) * p.obs_stage;
                 float* mine = wst + (gib & (G - 1)) * ND;
+                MRSIM_DCHECK(((gib & (G - 1)) + 1) * ND <= p.obs_stage);
                 for (int q = lane, r = lane / p.D, f = lane - (lane / p.D) * p.D; q < ND; q += L) {
                     mine[q] = static_cast<float>(obs_feature<TASK, Real>(c, view, r, f, p.bdim));
                     for (f += L; f >= p.D; f -= p.D) ++r;
@@ -873,6 +928,7 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
                 const long long left = p.e_end - e0;
                 const int total = static_cast<int>(left < G ? left : G) * ND;
                 float* dst = obs_s + e0 * ND;
+                MRSIM_DCHECK(total <= p.obs_stage && e0 * ND + total <= p.B * ND);
                 if (((e0 * ND) & 3) == 0 && (total & 3) == 0) {
                     const float4* src4 = reinterpret_cast<const float4*>(wst);
                     float4* dst4 = reinterpret_cast<float4*>(dst);
@@ -945,6 +1001,10 @@ __global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(co
             }
             Grp<L>::sync();
         }  // rollout steps
+#if MRSIM_GUARD_WORDS
+        Grp<L>::sync();
+        if (lane == 0) sm.guards(false, N, p.nf, p.ni, GroupSmem<Real>::rc_reals(L, MP, MO));
+#endif
 #ifdef MRSIM_TASK_STATS  // diagnostic builds: histogram of warp-task durations (log2 of SM cycles)
         if ((threadIdx.x & 31) == 0) {
             const long long dt = clock64() - t_task0;

@@ -46,6 +46,10 @@ print("device step (int8 acts)   %.1f us" % t(lambda: gb.step(da[nxt()])))
 print("host step, no outputs     %.1f us" % t(lambda: m.lib().mrsim_step_host(
     gb._h, acts[nxt()].ctypes.data_as(P), None, None, None, None)))
 print("host step, all outputs    %.1f us" % t(lambda: gb.step_host(acts[nxt()], out=outs)))
+print("host step, obs only       %.1f us" % t(lambda: m.lib().mrsim_step_host(
+    gb._h, acts[nxt()].ctypes.data_as(P), outs[0].ctypes.data, None, None, None)))
+print("host step, reward+done    %.1f us" % t(lambda: m.lib().mrsim_step_host(
+    gb._h, acts[nxt()].ctypes.data_as(P), None, outs[1].ctypes.data, outs[2].ctypes.data, None)))
 src = torch.empty((B, 4, cfg.obs_dim), dtype=torch.float32, device="cuda")
 dst = torch.empty((B, 4, cfg.obs_dim), dtype=torch.float32).pin_memory()
 print("pinned D2H 5.2 MB         %.1f us" % t(lambda: (dst.copy_(src, non_blocking=True), torch.cuda.synchronize())))
