@@ -42,6 +42,7 @@ struct mrsim_ctx {
     unsigned long long* d_err = nullptr;
     long long* d_err_serial = nullptr;
     unsigned* d_ticket = nullptr;
+    unsigned* d_exit = nullptr;  // step kernel's finished-warp counter (err_epilogue)
     long long scripted_launches = 0;
     int cur = 0;
     long long serial = 0;
@@ -437,6 +438,8 @@ StepParams<Real> step_params(mrsim_ctx* ctx, DevState<Real>* s, const int8_t* ac
     p.err_serial = ctx->d_err_serial;
     p.ticket = ctx->d_ticket;
     p.serial = ctx->serial;
+    p.exit_count = ctx->d_exit;
+    p.err_host = nullptr;
     p.B = ctx->B;
     p.e_begin = 0;
     p.e_end = ctx->B;
@@ -469,8 +472,9 @@ void step_done(mrsim_ctx* ctx) {
 template <class Real>
 int do_step(mrsim_ctx* ctx, DevState<Real>* s, const int8_t* actions, float* obs, float* reward, uint8_t* done,
             float* next_obs, cudaStream_t stream, double* reward64 = nullptr, const int32_t* actions32 = nullptr,
-            bool stage_obs = false) {
+            bool stage_obs = false, unsigned long long* err_host = nullptr) {
     StepParams<Real> p = step_params<Real>(ctx, s, actions, obs, reward, done, next_obs, reward64, actions32);
+    p.err_host = ctx->L > 1 ? err_host : nullptr;  // the env kernel has no epilogue: caller copies the word
     // warp-staged obs stores only where they pay: obs going straight to pinned host memory
     // (device-memory obs: ~2 % slower staged, measured)
     p.obs_stage = (stage_obs || ctx->L == 1 || MRSIM_STAGE_DEVICE_OBS) ? ctx->obs_stage : 0;
@@ -946,10 +950,12 @@ int mrsim_create(const mrsim_cfg* cfg, int device, int64_t num_envs, uint32_t fl
         cudaMemcpy(st.min_dist, inf.data(), 8 * ctx->B, cudaMemcpyHostToDevice);
     }
     // error word, its step serial, then the step kernel's two warp-task counters
-    if ((e = ctx_malloc(ctx, &ctx->d_err, 32)) != cudaSuccess) return bail(e, "cudaMalloc err");
+    if ((e = ctx_malloc(ctx, &ctx->d_err, 64)) != cudaSuccess) return bail(e, "cudaMalloc err");
     ctx->d_err_serial = reinterpret_cast<long long*>(ctx->d_err + 1);
     ctx->d_ticket = reinterpret_cast<unsigned*>(ctx->d_err + 2);  // step kernel [2], scripted kernel [2]
     cudaMemset(ctx->d_ticket, 0, 16);
+    ctx->d_exit = reinterpret_cast<unsigned*>(ctx->d_err + 4);
+    cudaMemset(ctx->d_exit, 0, 4);
     const unsigned long long none = ~0ull;
     cudaMemcpy(ctx->d_err, &none, sizeof none, cudaMemcpyHostToDevice);
     cudaMemset(ctx->d_err_serial, 0xff, 8);
@@ -1154,18 +1160,27 @@ int mrsim_step_host(mrsim_ctx* ctx, const int32_t* actions_host, float* obs_host
     // The reference's std::vector<int> goes up as is; validate_actions (batch.hpp:226-237) runs in the
     // step kernel (first offender in (env, robot) order wins), and a failing step is rolled back below.
     const bool zero_copy_obs = obs && obs != ctx->d_obs;
+    // error word + serial: written into pinned memory by the step kernel's last warp (no copy
+    // after the kernel); a sentinel left in place means it was not (env kernel): copy it
+    if (!ctx->h_err) CK(cudaMallocHost(&ctx->h_err, 16));
+    constexpr unsigned long long kUnwritten = ~0ull - 1;
+    volatile unsigned long long* herr = ctx->h_err;
+    herr[0] = kUnwritten;
+    unsigned long long* err_dev = mapped_alias(ctx->h_err);
     const int rc = ctx->fp64 ? do_step<double>(ctx, ctx->sd, nullptr, obs, nullptr, done, nullptr, s, rew, act,
-                                               zero_copy_obs)
+                                               zero_copy_obs, err_dev)
                              : do_step<float>(ctx, ctx->sf, nullptr, obs, nullptr, done, nullptr, s, rew, act,
-                                              zero_copy_obs);
+                                              zero_copy_obs, err_dev);
     if (rc != MRSIM_OK) return rc;
     if (obs_host && obs == ctx->d_obs) CK(cudaMemcpyAsync(obs_host, obs, obs_bytes, cudaMemcpyDeviceToHost, s));
     if (reward_host && rew == ctx->d_reward64)
         CK(cudaMemcpyAsync(reward_host, rew, 8 * ctx->B, cudaMemcpyDeviceToHost, s));
     if (done_host && done == ctx->d_done) CK(cudaMemcpyAsync(done_host, done, ctx->B, cudaMemcpyDeviceToHost, s));
-    if (!ctx->h_err) CK(cudaMallocHost(&ctx->h_err, 16));
-    CK(cudaMemcpyAsync(ctx->h_err, ctx->d_err, 16, cudaMemcpyDeviceToHost, s));  // error word + serial
     CK(cudaStreamSynchronize(s));
+    if (herr[0] == kUnwritten) {
+        CK(cudaMemcpy(ctx->h_err, ctx->d_err, 16, cudaMemcpyDeviceToHost));
+        CK(cudaMemset(ctx->d_exit, 0, 4));  // in case a launch ended without its epilogue
+    }
     return check_device_error(ctx, true, actions_host, ctx->h_err);
 }
 
