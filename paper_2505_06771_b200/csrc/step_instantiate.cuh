@@ -247,4 +247,8 @@ extern "C" int MRSIM_DBG_CAT(mrsim_debug_task_hist_task, MRSIM_TASK_ID)(unsigned
     }
     return 0;
 }
+extern "C" int MRSIM_DBG_CAT(mrsim_debug_warp_log_task, MRSIM_TASK_ID)(unsigned long long* out, int n_warps) {
+    if (n_warps > mrsim_dev::kWarpLogMax) n_warps = mrsim_dev::kWarpLogMax;
+    return cudaMemcpyFromSymbol(out, mrsim_dev::g_warp_log, 40 * n_warps) != cudaSuccess;
+}
 #endif

@@ -575,6 +575,14 @@ __device__ __forceinline__ Real wrap_angle_dev(Real t) {
 
 #ifdef MRSIM_TASK_STATS
 __device__ unsigned long long g_task_hist[64];
+// per warp of the last launch: entry, first task start, last task end, busy time (globaltimer ns), tasks
+constexpr int kWarpLogMax = 8192;
+__device__ unsigned long long g_warp_log[kWarpLogMax * 5];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 #endif
 
 template <class Real>
@@ -666,6 +674,10 @@ __device__ __forceinline__ void step_body(const StepParams<Real>& p) {
     const EnvView<Real> view{sm.xs, sm.ys, sm.ts, sm.tf, sm.ti, N, sm.drones, p.prey_off,
                              TASK == MRSIM_TASK_ARCTIC_TRANSPORT ? sm.dcell : nullptr, het_flat};
     const long long stride = static_cast<long long>(gridDim.x) * gpb;
+#ifdef MRSIM_TASK_STATS
+    const unsigned long long w_enter = gtimer();
+    unsigned long long w_first = 0, w_last = 0, w_busy = 0, w_tasks = 0;
+#endif
 
     auto next_task = [&](long long e_static) -> long long {
         if (!MRSIM_DYN_SCHED) return e_static;
@@ -686,6 +698,8 @@ __device__ __forceinline__ void step_body(const StepParams<Real>& p) {
 #endif
 #ifdef MRSIM_TASK_STATS
         const long long t_task0 = clock64();
+        const unsigned long long g_task0 = gtimer();
+        if (w_first == 0) w_first = g_task0;
 #endif
         // mrsim_rollout: n_steps consecutive steps of the task's envs in this launch. Step 0 reads
         // the input copy, later steps update the output copy in place (each env belongs to this
@@ -1014,8 +1028,24 @@ __device__ __forceinline__ void step_body(const StepParams<Real>& p) {
             atomicAdd(&g_task_hist[b < 47 ? b : 47], 1ull);
             atomicAdd(&g_task_hist[48], static_cast<unsigned long long>(dt));
         }
+        w_last = gtimer();
+        w_busy += w_last - g_task0;
+        ++w_tasks;
 #endif
     }
+#ifdef MRSIM_TASK_STATS
+    {
+        const unsigned wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+        if ((threadIdx.x & 31) == 0 && wid < kWarpLogMax) {
+            unsigned long long* o = g_warp_log + 5 * wid;
+            o[0] = w_enter;
+            o[1] = w_first;
+            o[2] = w_last;
+            o[3] = w_busy;
+            o[4] = w_tasks;
+        }
+    }
+#endif
 }
 
 // Host-API steps: the last warp of the launch to finish copies the error word and its serial into
