@@ -167,44 +167,41 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
             //    logical order: M is SPD and the j-th pivot is the Schur complement |z|^2 the bordered
             //    update of row j would see, so `pivot <= eps_z` is the cold path's dependence test
             const bool w0 = wok && lp0 >= 0, w1 = wok && lp1 >= 0;
+            // the warm set occupies physical slots [0, kw): counted loops (no mask walks)
+            const int kw = wok ? wk : 0;
             if (w0)
-                for (unsigned m = amask; m; m &= m - 1) {
-                    const int c = __ffs(m) - 1;
-                    ws.S[q0 * n + c] = rows.dot(ws.desc[q0], ws.desc[c]);
-                }
+                for (int c = 0; c < kw; ++c) ws.S[q0 * n + c] = rows.dot(ws.desc[q0], ws.desc[c]);
             if (w1)
-                for (unsigned m = amask; m; m &= m - 1) {
-                    const int c = __ffs(m) - 1;
-                    ws.S[q1 * n + c] = rows.dot(ws.desc[q1], ws.desc[c]);
-                }
+                for (int c = 0; c < kw; ++c) ws.S[q1 * n + c] = rows.dot(ws.desc[q1], ws.desc[c]);
             for (int pv = 0; pv < wmax; ++pv) {
                 Grp<L>::sync();
                 const bool act = wok && pv < wk;
                 const Real piv = act ? ws.S[pv * n + pv] : Real(1);
                 if (act && !(piv > Prec<Real>::eps_z)) wok = false;  // dependent now: cold start
                 const bool go = act && wok;
+                Real* const prow = ws.S + pv * n;
                 if (go && lane == pv % L) {  // scale the pivot row
                     const Real ip = Real(1) / piv;
-                    for (unsigned m = amask; m; m &= m - 1) {
-                        const int c = __ffs(m) - 1;
-                        ws.S[pv * n + c] = (c == pv) ? ip : ws.S[pv * n + c] * ip;
-                    }
+#pragma unroll 4
+                    for (int c = 0; c < kw; ++c) prow[c] *= ip;
+                    prow[pv] = ip;
                 }
                 Grp<L>::sync();
                 if (go) {  // eliminate the pivot column from the other rows
+                    const Real ipv = prow[pv];
                     if (w0 && q0 != pv) {
-                        const Real f = ws.S[q0 * n + pv];
-                        for (unsigned m = amask; m; m &= m - 1) {
-                            const int c = __ffs(m) - 1;
-                            ws.S[q0 * n + c] = (c == pv) ? -f * ws.S[pv * n + pv] : ws.S[q0 * n + c] - f * ws.S[pv * n + c];
-                        }
+                        Real* const row = ws.S + q0 * n;
+                        const Real f = row[pv];
+#pragma unroll 4
+                        for (int c = 0; c < kw; ++c) row[c] = row[c] - f * prow[c];
+                        row[pv] = -f * ipv;
                     }
                     if (w1 && q1 != pv) {
-                        const Real f = ws.S[q1 * n + pv];
-                        for (unsigned m = amask; m; m &= m - 1) {
-                            const int c = __ffs(m) - 1;
-                            ws.S[q1 * n + c] = (c == pv) ? -f * ws.S[pv * n + pv] : ws.S[q1 * n + c] - f * ws.S[pv * n + c];
-                        }
+                        Real* const row = ws.S + q1 * n;
+                        const Real f = row[pv];
+#pragma unroll 4
+                        for (int c = 0; c < kw; ++c) row[c] = row[c] - f * prow[c];
+                        row[pv] = -f * ipv;
                     }
                 }
             }
@@ -217,17 +214,11 @@ __device__ __forceinline__ int qp_solve(const Grp<L>& g, RowSet& rows, const QpW
             Grp<L>::sync();
             Real l0 = 0, l1 = 0;
             if (w0 && wok) {
-                for (unsigned m = amask; m; m &= m - 1) {
-                    const int c = __ffs(m) - 1;
-                    l0 += ws.S[q0 * n + c] * ws.d[c];
-                }
+                for (int c = 0; c < kw; ++c) l0 += ws.S[q0 * n + c] * ws.d[c];
                 ws.lam[q0] = l0;
             }
             if (w1 && wok) {
-                for (unsigned m = amask; m; m &= m - 1) {
-                    const int c = __ffs(m) - 1;
-                    l1 += ws.S[q1 * n + c] * ws.d[c];
-                }
+                for (int c = 0; c < kw; ++c) l1 += ws.S[q1 * n + c] * ws.d[c];
                 ws.lam[q1] = l1;
             }
             // 3) dual feasibility of the warm point, else the cold start
