@@ -20,9 +20,11 @@
 #include "qp_group.cuh"
 #include "tasks.cuh"
 
-// 128-thread blocks per SM the register budget is sized for (measured on B200:
-// 4 -> <=128 regs is best for L <= 8; 3 -> <=168 regs for the QP-heavy L = 16
-// and for rware, whose obstacle rows spill at 128 regs: +21% / +18% at N = 4 / 6).
+// 128-thread blocks per SM the register budget is sized for (measured on B200): 4 -> <= 128 regs
+// for L <= 8 and for L = 16 with up to 3 pair slots (N <= 10: arctic +8 %, MT +13 % over 3 since
+// the counted warm-start loops, profiles/r02/ab_l16_minblocks.log); 3 -> <= 168 regs for wider
+// L = 16 teams (N > 10, which spill at 128) and for rware, whose obstacle rows spill at 128 regs
+// (+21% / +18% at N = 4 / 6). Shared memory caps the bench configurations at 4 blocks anyway.
 #ifndef MRSIM_RW_MINB
 #define MRSIM_RW_MINB 3
 #endif
@@ -30,7 +32,8 @@
 #define MRSIM_SMALL_MINB 4
 #endif
 #ifndef MRSIM_MIN_BLOCKS
-#define MRSIM_MIN_BLOCKS(L, TASK) ((L) >= 16 ? 3 : (TASK) == MRSIM_TASK_RWARE ? MRSIM_RW_MINB : MRSIM_SMALL_MINB)
+#define MRSIM_MIN_BLOCKS(L, MP, TASK) \
+    ((L) >= 16 ? ((MP) <= 3 ? 4 : 3) : (TASK) == MRSIM_TASK_RWARE ? MRSIM_RW_MINB : MRSIM_SMALL_MINB)
 #endif
 
 namespace mrsim_dev {
@@ -1069,7 +1072,7 @@ __device__ __forceinline__ void err_epilogue(const StepParams<Real>& p) {
 }
 
 template <class Real, int L, int MP, int MO, int TASK, bool MULTI = false>
-__global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, TASK)) step_kernel(const __grid_constant__ StepParams<Real> p) {
+__global__ void __launch_bounds__(128, MRSIM_MIN_BLOCKS(L, MP, TASK)) step_kernel(const __grid_constant__ StepParams<Real> p) {
     step_body<Real, L, MP, MO, TASK, MULTI>(p);
     if (p.err_host) err_epilogue(p);
 }
