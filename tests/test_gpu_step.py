@@ -222,10 +222,12 @@ def test_free_running_horizon_matches_reference(task, n, fp64, ref):
         assert len(diverged) <= (3 * B) // 4, sorted(diverged)
 
 
-def test_invalid_action_reports_env_and_robot_and_rolls_back():
-    # test_framework.cpp:171-185
+@pytest.mark.parametrize("env_per_thread", [False, True])
+def test_invalid_action_reports_env_and_robot_and_rolls_back(env_per_thread):
+    # test_framework.cpp:171-185. The lane-group kernel's last warp hands the error word to the
+    # host step in pinned memory; the env kernel has no such epilogue (the host copies the word).
     cfg = m.make_default_config("navigation")
-    gb = m.CudaEnvBatch(cfg, 2)
+    gb = m.CudaEnvBatch(cfg, 2, env_per_thread=env_per_thread)
     gb.reset_seeds([5, 6])
     before = gb.get_states()
     with pytest.raises(m.InvalidArgument, match=r"environment 0, robot 1"):
@@ -233,6 +235,28 @@ def test_invalid_action_reports_env_and_robot_and_rolls_back():
     after = gb.get_states()
     assert [s.x[0] for s in before] == [s.x[0] for s in after]
     gb.step_host([0] * 6)  # context stays usable
+
+
+@pytest.mark.parametrize("env_per_thread", [False, True])
+def test_host_step_reports_an_earlier_queued_failure(env_per_thread):
+    """A failing asynchronous device step, then a host step: the host step's launch is a no-op
+    (sticky word) whose last warp still hands the word over; the error of the earlier step is
+    raised and the state rolled back to that step's input."""
+    import torch
+    cfg = m.make_default_config("navigation")
+    gb = m.CudaEnvBatch(cfg, 40, env_per_thread=env_per_thread)
+    gb.reset_seeds(list(range(40)))
+    before = gb.get_states()
+    bad = torch.zeros((40, 3), dtype=torch.int8, device="cuda")
+    bad[23, 2] = 6
+    gb.step(bad)
+    with pytest.raises(m.InvalidArgument, match=r"environment 23, robot 2"):
+        gb.step_host([0] * 120)
+    after = gb.get_states()
+    assert [list(s.x[:3]) for s in before] == [list(s.x[:3]) for s in after]
+    assert [s.step_index for s in before] == [s.step_index for s in after]
+    gb.step_host([0] * 120)  # usable again
+    assert gb.get_states(0, 1)[0].step_index == before[0].step_index + 1
 
 
 def test_device_invalid_action_is_sticky_then_rolled_back():
