@@ -67,7 +67,7 @@ def parse():
                     help="teams of <= 4 robots: one thread per env instead of the lane-per-robot kernel (A/B)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
-    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--e2e-steps", type=int, default=40)
     ap.add_argument("--dist-backend", default="auto",
                     help="nccl | gloo | auto (nccl when every rank has its own GPU, else gloo)")
     ap.add_argument("--controller", default="unicycle_position", choices=["unicycle_position", "unicycle_pose"],
@@ -454,14 +454,17 @@ def main():
     if a.e2e_steps > 0:
         rng = np.random.default_rng(rank)
         # pinned host buffers: the step's inputs (the reference's int actions) and its outputs
-        acts = torch.from_numpy(rng.integers(0, 5, size=(a.e2e_steps, B, a.robots), dtype=np.int32)).pin_memory()
+        n_warm = max(3, a.warmup)  # untimed host steps first, like the device-timed loop
+        acts = torch.from_numpy(rng.integers(0, 5, size=(a.e2e_steps + n_warm, B, a.robots),
+                                             dtype=np.int32)).pin_memory()
         acts_np = acts.numpy()
         outs = (torch.empty((B, a.robots, cfg.obs_dim), dtype=torch.float32).pin_memory().numpy(),
                 torch.empty((B,), dtype=torch.float64).pin_memory().numpy(),
                 torch.empty((B,), dtype=torch.uint8).pin_memory().numpy())
         hb = m.CudaEnvBatch(cfg, B, device=local, fp64=(not a.fp32), auto_reset=True, env_per_thread=a.env_per_thread)
         hb.reset_episodes(root_seed=0, first_episode=shard.first_episode, episode_stride=shard.episode_stride)
-        hb.step_host(acts_np[0], out=outs)
+        for k in range(n_warm):
+            hb.step_host(acts_np[a.e2e_steps + k], out=outs)
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
