@@ -341,9 +341,9 @@ def test_host_api_matches_device_step(pinned):
 
 
 # Every kernel variant and the extremes of the team size: N = 1 (no pair rows), 2, 7 (L=8, 4 pair
-# slots per lane), 13 and 16 (L=16, 8 pair slots; 16 = MRSIM_MAX_ROBOTS), and rware with 8 slots
-# (the 16-obstacle-slot variant).
-@pytest.mark.parametrize("n", [1, 2, 7, 13, 16])
+# slots per lane), 9 (L=16, 3 pair slots: the 4-blocks-per-SM build), 13 and 16 (L=16, 8 pair
+# slots; 16 = MRSIM_MAX_ROBOTS), and rware with 8 slots (the 16-obstacle-slot variant).
+@pytest.mark.parametrize("n", [1, 2, 7, 9, 13, 16])
 def test_team_size_extremes_match_reference(n, ref):
     cfg, st = _teacher_forced(ref, "navigation", n, True, 0, 40, B=24)
     assert st["discrete"] == [], st["discrete"][:5]
