@@ -55,6 +55,7 @@ struct mrsim_ctx {
     int num_sms = 148;
     int block = 128;
     int grid = 0;
+    int grid_staged = 0;  // the grid of launches with the warp obs stage (host-buffer steps)
     int smem_group = 0;
     int obs_stage = 0;  // floats per warp of the staged obs store (0: direct stores)
     // host-API scratch
@@ -479,7 +480,8 @@ int do_step(mrsim_ctx* ctx, DevState<Real>* s, const int8_t* actions, float* obs
     // (device-memory obs: ~2 % slower staged, measured)
     p.obs_stage = (stage_obs || ctx->L == 1 || MRSIM_STAGE_DEVICE_OBS) ? ctx->obs_stage : 0;
     const int smem = ctx->smem_group * (ctx->block / ctx->L) + 4 * p.obs_stage * (ctx->block / 32);
-    cudaError_t e = dispatch_step<Real>(ctx->cfg.task, p, ctx->var, ctx->grid, ctx->block, smem, stream);
+    const int grid = (p.obs_stage && ctx->L > 1) ? ctx->grid_staged : ctx->grid;
+    cudaError_t e = dispatch_step<Real>(ctx->cfg.task, p, ctx->var, grid, ctx->block, smem, stream);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "step kernel launch");
     step_done(ctx);
     return MRSIM_OK;
@@ -965,6 +967,7 @@ int mrsim_create(const mrsim_cfg* cfg, int device, int64_t num_envs, uint32_t fl
         ctx->obs_stage = stage <= mrsim_dev::kEnvObsStageMax ? stage : 0;
         ctx->smem_group = 0;
         ctx->grid = static_cast<int>((ctx->B + ctx->block - 1) / ctx->block);
+        ctx->grid_staged = ctx->grid;
         int bps = 0;
         const int smem = 4 * ctx->obs_stage * (ctx->block / 32);
         e = ctx->fp64 ? dispatch_occ<double>(cfg->task, ctx->var, ctx->block, smem, &bps)
@@ -985,7 +988,11 @@ int mrsim_create(const mrsim_cfg* cfg, int device, int64_t num_envs, uint32_t fl
     if (e != cudaSuccess) return bail(e, "occupancy query");
     if (bps < 1) bps = 1;
     // Warp-staged observation stores (one contiguous block per warp, full-line writes; what makes
-    // zero-copy obs to pinned host memory efficient): on when it costs no occupancy.
+    // zero-copy obs to pinned host memory efficient), used by host-buffer steps only. On when it
+    // costs no occupancy, and also when it costs one resident block: the host link is then the
+    // bound (e2e: discovery N=6 +75 %, rware N=6 +64 %, MT N=10 +28 %) — except for arctic_transport,
+    // whose QP-heavy step loses more to the missing block (-14 %; profiles/r02/ab_host_stage.log).
+    int bps_staged = bps;
     {
         const int stage = (((32 / ctx->L) * ctx->N * ctx->D + 3) / 4) * 4;  // floats per warp (16-B multiple)
         const int smem2 = smem + 4 * stage * (ctx->block / 32);
@@ -993,12 +1000,17 @@ int mrsim_create(const mrsim_cfg* cfg, int device, int64_t num_envs, uint32_t fl
         e = ctx->fp64 ? dispatch_occ<double>(cfg->task, ctx->var, ctx->block, smem2, &bps2)
                       : dispatch_occ<float>(cfg->task, ctx->var, ctx->block, smem2, &bps2);
         if (e != cudaSuccess) return bail(e, "occupancy query");
-        ctx->obs_stage = (bps2 >= bps) ? stage : 0;
+        const bool free = bps2 >= bps;
+        const bool worth = bps2 >= 1 && bps2 + 1 >= bps && cfg->task != MRSIM_TASK_ARCTIC_TRANSPORT;
+        ctx->obs_stage = (free || worth) ? stage : 0;
+        if (!free && worth) bps_staged = bps2;
     }
     const long long gpb = ctx->block / ctx->L;
     const long long need = (ctx->B + gpb - 1) / gpb;
     const long long full = static_cast<long long>(ctx->num_sms) * bps;
+    const long long full_staged = static_cast<long long>(ctx->num_sms) * bps_staged;
     ctx->grid = static_cast<int>(need < full ? need : full);
+    ctx->grid_staged = static_cast<int>(need < full_staged ? need : full_staged);
     if ((e = cudaDeviceSynchronize()) != cudaSuccess) return bail(e, "create sync");
     *out = ctx;
     return MRSIM_OK;
