@@ -58,6 +58,7 @@ struct mrsim_ctx {
     int grid_staged = 0;  // the grid of launches with the warp obs stage (host-buffer steps)
     int smem_group = 0;
     int obs_stage = 0;  // floats per warp of the staged obs store (0: direct stores)
+    bool obs_ws_ok = false;  // an env's obs fit its group's QP inverse-Gram matrix (the fallback stage)
     // host-API scratch
     float* d_obs = nullptr;
     double* d_reward64 = nullptr;
@@ -479,6 +480,7 @@ int do_step(mrsim_ctx* ctx, DevState<Real>* s, const int8_t* actions, float* obs
     // warp-staged obs stores only where they pay: obs going straight to pinned host memory
     // (device-memory obs: ~2 % slower staged, measured)
     p.obs_stage = (stage_obs || ctx->L == 1 || MRSIM_STAGE_DEVICE_OBS) ? ctx->obs_stage : 0;
+    p.obs_ws_stage = (stage_obs && ctx->L > 1 && !p.obs_stage && ctx->obs_ws_ok) ? 1 : 0;
     const int smem = ctx->smem_group * (ctx->block / ctx->L) + 4 * p.obs_stage * (ctx->block / 32);
     const int grid = (p.obs_stage && ctx->L > 1) ? ctx->grid_staged : ctx->grid;
     cudaError_t e = dispatch_step<Real>(ctx->cfg.task, p, ctx->var, grid, ctx->block, smem, stream);
@@ -989,9 +991,12 @@ int mrsim_create(const mrsim_cfg* cfg, int device, int64_t num_envs, uint32_t fl
     if (bps < 1) bps = 1;
     // Warp-staged observation stores (one contiguous block per warp, full-line writes; what makes
     // zero-copy obs to pinned host memory efficient), used by host-buffer steps only. On when it
-    // costs no occupancy, and also when it costs one resident block: the host link is then the
-    // bound (e2e: discovery N=6 +75 %, rware N=6 +64 %, MT N=10 +28 %) — except for arctic_transport,
-    // whose QP-heavy step loses more to the missing block (-14 %; profiles/r02/ab_host_stage.log).
+    // costs no occupancy, and also when it costs one of 4 resident blocks: the host link is then the
+    // bound (e2e over direct stores: discovery N=6 +75 %, MT N=10 +28 %, foraging N=6) — except for
+    // arctic_transport, whose QP-heavy step loses more to the missing block (-14 %). Otherwise each
+    // env's obs are staged in its group's dead QP matrix (no extra smem): arctic N=10 +22 %, and
+    // rware N=6 (3 -> 2 blocks with the warp stage) +8 % over the warp stage
+    // (profiles/r02/ab_host_stage.log).
     int bps_staged = bps;
     {
         const int stage = (((32 / ctx->L) * ctx->N * ctx->D + 3) / 4) * 4;  // floats per warp (16-B multiple)
@@ -1001,9 +1006,12 @@ int mrsim_create(const mrsim_cfg* cfg, int device, int64_t num_envs, uint32_t fl
                       : dispatch_occ<float>(cfg->task, ctx->var, ctx->block, smem2, &bps2);
         if (e != cudaSuccess) return bail(e, "occupancy query");
         const bool free = bps2 >= bps;
-        const bool worth = bps2 >= 1 && bps2 + 1 >= bps && cfg->task != MRSIM_TASK_ARCTIC_TRANSPORT;
+        const bool worth = bps2 >= 3 && bps2 + 1 >= bps && cfg->task != MRSIM_TASK_ARCTIC_TRANSPORT;
         ctx->obs_stage = (free || worth) ? stage : 0;
         if (!free && worth) bps_staged = bps2;
+        // otherwise stage each env's obs in its group's dead QP inverse-Gram matrix (no extra smem)
+        const long long nd = static_cast<long long>(ctx->N) * ctx->D;
+        ctx->obs_ws_ok = (nd % 2) == 0 && nd * 4 <= 4ll * ctx->N * ctx->N * (ctx->fp64 ? 8 : 4);
     }
     const long long gpb = ctx->block / ctx->L;
     const long long need = (ctx->B + gpb - 1) / gpb;

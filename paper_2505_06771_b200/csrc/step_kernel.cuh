@@ -131,6 +131,7 @@ struct StepParams {
     long long episode_stride;
     int smem_bytes_per_group;
     int obs_stage;  // floats per warp of the obs staging buffer after the group regions (0: direct stores)
+    int obs_ws_stage;  // 1: stage each env's obs in its group's QP workspace instead (host-buffer steps)
     PhysConsts<Real> k;
     double prey_off[16];  // predator_prey candidate offsets (host-computed with the reference's libm)
 };
@@ -954,6 +955,27 @@ __device__ __forceinline__ void step_body(const StepParams<Real>& p) {
                     for (int k = threadIdx.x & 31; k < total / 4; k += 32) dst4[k] = src4[k];
                 } else {
                     for (int k = threadIdx.x & 31; k < total; k += 32) dst[k] = wst[k];
+                }
+                __syncwarp();
+            } else if (obs_s && p.obs_ws_stage) {
+                // host-buffer steps whose warp stage would cost a resident block: each group stages
+                // its env's obs in its own QP inverse-Gram matrix (dead after the ticks), and the warp
+                // stores its consecutive envs' block as 8-byte pieces (256 contiguous bytes per store)
+                float* mine = reinterpret_cast<float*>(sm.qp.S);
+                MRSIM_DCHECK(ND * 4 <= 4 * N * N * static_cast<int>(sizeof(Real)) && (ND & 1) == 0);
+                for (int q = lane, r = lane / p.D, f = lane - (lane / p.D) * p.D; q < ND; q += L) {
+                    mine[q] = static_cast<float>(obs_feature<TASK, Real>(c, view, r, f, p.bdim));
+                    for (f += L; f >= p.D; f -= p.D) ++r;
+                }
+                __syncwarp();
+                const long long left = p.e_end - e0;
+                const int half = ND / 2;  // float2 per env
+                const int total2 = static_cast<int>(left < G ? left : G) * half;
+                const unsigned char* wbase = smem_raw + (gib & ~(G - 1)) * p.smem_bytes_per_group;
+                float2* dst2 = reinterpret_cast<float2*>(obs_s + e0 * ND);
+                for (int k = threadIdx.x & 31; k < total2; k += 32) {
+                    const int g2 = k / half;
+                    dst2[k] = reinterpret_cast<const float2*>(wbase + g2 * p.smem_bytes_per_group)[k - g2 * half];
                 }
                 __syncwarp();
             } else if (obs_s && !skip) {

@@ -340,6 +340,40 @@ def test_host_api_matches_device_step(pinned):
     assert ga.get_states(40000, 1)[0].x[0] == before
 
 
+@pytest.mark.parametrize("task,n", [("navigation", 4), ("discovery", 6), ("rware", 6), ("material_transport", 10),
+                                    ("arctic_transport", 10)])
+def test_host_step_obs_staging_matches_device_step(task, n):
+    """Every obs path of the pinned host step equals the device-buffer step: the warp stage when it
+    is free (navigation), when it costs a resident block (discovery, rware N=6, MT N=10: smaller
+    grid) and the QP-workspace stage (arctic N=10); B odd, so the last warp task is partial."""
+    import torch
+    cfg = m.make_default_config(task)
+    if n != cfg.raw.num_robots:
+        cfg.set_num_robots(n, tile_roster=cfg.raw.het_rows > 0)
+    if task == "arctic_transport":
+        cfg.set_layout("arctic.spawn_zone", [-1.55, -1.05, -0.9, 0.9])
+    B = 3001
+    seeds = [m.derive_episode_seed(5, e) for e in range(B)]
+    ga, gb = m.CudaEnvBatch(cfg, B), m.CudaEnvBatch(cfg, B)
+    ga.reset_seeds(seeds)
+    gb.reset_seeds(seeds)
+    rng = np.random.default_rng(1)
+    pin = lambda shape, dt: torch.empty(shape, dtype=dt).pin_memory().numpy()  # noqa: E731
+    outs = (pin((B, n, cfg.obs_dim), torch.float32), pin((B,), torch.float64), pin((B,), torch.uint8))
+    acts = pin((B, n), torch.int32)
+    for _ in range(4):
+        acts[:] = rng.integers(0, 5, size=(B, n), dtype=np.int32)
+        obs, rew, done = ga.step_host(acts, out=outs)
+        out = gb.step(torch.from_numpy(acts.astype(np.int8)).cuda())
+        torch.cuda.synchronize()
+        assert np.array_equal(obs, out.obs.cpu().numpy())
+        assert np.array_equal(rew.astype(np.float32), out.reward.cpu().numpy())
+        assert np.array_equal(done, out.done.cpu().numpy())
+    sa, sb = ga.get_states(), gb.get_states()
+    for e in (0, 1, B // 2, B - 2, B - 1):
+        assert list(sa[e].x[:n]) == list(sb[e].x[:n]) and sa[e].step_index == sb[e].step_index
+
+
 # Every kernel variant and the extremes of the team size: N = 1 (no pair rows), 2, 7 (L=8, 4 pair
 # slots per lane), 9 (L=16, 3 pair slots: the 4-blocks-per-SM build), 13 and 16 (L=16, 8 pair
 # slots; 16 = MRSIM_MAX_ROBOTS), and rware with 8 slots (the 16-obstacle-slot variant).
