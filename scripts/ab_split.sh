@@ -1,9 +1,12 @@
 #!/bin/bash
-# Split steps (two half-step warp tasks per env group; default when the batch is < 8 task rounds) vs whole steps
-# (MRSIM_SPLIT=0), same library.
-run() { MRSIM_SPLIT=$1 timeout 300 python bench.py --steps 40 --warmup 5 --no-cpu-baseline --e2e-steps 40 --rollout 0 ${@:2} 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('value %.4g e2e %.4g' % (d['value'], d['e2e']['value']))" 2>&1 | tail -1; }
+# Split steps (half-step warp tasks; build/ab/lib_split.so with MRSIM_SPLIT=1) vs the same build whole-step vs the
+# shipped kernel, same box.
+run() { timeout 300 python bench.py --steps 40 --warmup 5 --no-cpu-baseline --e2e-steps 0 --rollout 0 "$@" 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('%.4g' % d['value'])" 2>&1 | tail -1; }
 for rep in 1 2; do
-for tn in navigation:4:65536:70 discovery:6:32768:100 predator_prey:6:32768:100 foraging:4:65536:100 navigation:4:16384:70; do
+for tn in navigation:4:65536:70 discovery:6:32768:100 predator_prey:6:32768:100; do
   IFS=: read t n e h <<< "$tn"
-  echo "$t N=$n B=$e: whole $(run 0 --task $t --robots $n --envs $e --max-steps $h) | split $(run 1 --task $t --robots $n --envs $e --max-steps $h)"
+  a=$(run --task $t --robots $n --envs $e --max-steps $h)
+  b=$(MRSIM_LIB_PATH=build/ab/lib_split.so run --task $t --robots $n --envs $e --max-steps $h)
+  c=$(MRSIM_SPLIT=1 MRSIM_LIB_PATH=build/ab/lib_split.so run --task $t --robots $n --envs $e --max-steps $h)
+  echo "$t N=$n B=$e: shipped $a | split-build whole $b | split-build split $c"
 done; done
