@@ -4,6 +4,8 @@ scale_parity.run_full_batch: every env of an auto-reset device batch against the
 stepping the same envs across two episode waves (discrete fields bit-exact, poses 1e-8 m).
 Covers the combinations the targeted suites do not enumerate, on every lane-group variant
 (L = 4 / 8 / 16, with and without obstacle slots)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -11,6 +13,8 @@ from scale_parity import run_full_batch
 from test_gpu_step import make_cfgs
 
 pytestmark = pytest.mark.gpu
+# MRSIM_FUZZ_SCALE=k multiplies the number of cases (long sweeps: profiles/r02/fuzz_long.log)
+SCALE = int(os.environ.get("MRSIM_FUZZ_SCALE", "1"))
 
 # team sizes that every task's default layout can spawn (arctic N > 4 uses the wider spawn zone)
 N_RANGE = {"navigation": (1, 12), "predator_prey": (2, 8), "discovery": (2, 8), "rware": (1, 6),
@@ -29,7 +33,7 @@ def _draw(k: int):
 
 
 @pytest.mark.timeout(900)
-@pytest.mark.parametrize("k", range(72))
+@pytest.mark.parametrize("k", range(72 * SCALE))
 def test_random_configuration_matches_reference(k, ref):
     d = _draw(k)
     cfg, sp = make_cfgs(ref, d["task"], d["n"], max_steps=d["max_steps"], controller=d["controller"])
@@ -53,14 +57,14 @@ def _device_cfg(ref, d):
     return cfg
 
 
-@pytest.mark.parametrize("k", range(24))
+@pytest.mark.parametrize("k", range(24 * SCALE))
 def test_random_configuration_rollout_equals_single_steps(k, ref):
     """mrsim_rollout (T fused steps) == T mrsim_step calls, bit for bit, on random configurations."""
     import torch
 
     import paper_2505_06771_b200 as m
     from scale_parity import compare_arrays
-    d = _draw(500 + k)
+    d = _draw(5000 + k)
     cfg = _device_cfg(ref, d)
     T = 2 * d["max_steps"] + 3
     a = m.CudaEnvBatch(cfg, d["B"], fp64=True, auto_reset=True)
@@ -81,13 +85,13 @@ def test_random_configuration_rollout_equals_single_steps(k, ref):
     assert not c["discrete_mismatch"] and c["pose"] == 0 and c["real"] == 0, (d, c)
 
 
-@pytest.mark.parametrize("k", range(24))
+@pytest.mark.parametrize("k", range(24 * SCALE))
 def test_random_configuration_host_step_equals_device_step(k, ref):
     """The pinned host-buffer step (zero-copy, staged obs) == the device-buffer step."""
     import torch
 
     import paper_2505_06771_b200 as m
-    d = _draw(900 + k)
+    d = _draw(9000 + k)
     cfg = _device_cfg(ref, d)
     B, n = d["B"], d["n"]
     ga, gb = m.CudaEnvBatch(cfg, B), m.CudaEnvBatch(cfg, B)
