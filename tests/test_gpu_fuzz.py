@@ -82,7 +82,11 @@ def test_random_configuration_rollout_equals_single_steps(k, ref):
     b.sync()
     assert torch.equal(torch.stack(rew), ro.reward) and torch.equal(torch.stack(obs), ro.obs), d
     c = compare_arrays(a.get_states(), b.get_states(), d["n"])
-    assert not c["discrete_mismatch"] and c["pose"] == 0 and c["real"] == 0, (d, c)
+    # Bit-identity of the two kernel instantiations (single step, MULTI) holds on the shipped build;
+    # the device-checks build's asserts change FMA contraction in one of them, so there the fp64
+    # poses may differ in the last bit (discrete fields and the fp32 outputs stay identical).
+    ulp = 1e-14 if hasattr(m.lib(), "mrsim_debug_check_guards") else 0.0
+    assert not c["discrete_mismatch"] and c["pose"] <= ulp and c["angle"] <= 10 * ulp and c["real"] <= ulp, (d, c)
 
 
 @pytest.mark.parametrize("k", range(24 * SCALE))
