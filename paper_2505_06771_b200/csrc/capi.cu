@@ -1011,7 +1011,8 @@ int mrsim_create(const mrsim_cfg* cfg, int device, int64_t num_envs, uint32_t fl
         if (!free && worth) bps_staged = bps2;
         // otherwise stage each env's obs in its group's dead QP inverse-Gram matrix (no extra smem)
         const long long nd = static_cast<long long>(ctx->N) * ctx->D;
-        ctx->obs_ws_ok = (nd % 2) == 0 && nd * 4 <= 4ll * ctx->N * ctx->N * (ctx->fp64 ? 8 : 4);
+        ctx->obs_ws_ok = mrsim_dev::obs_ws_stage_task(cfg->task) && (nd % 2) == 0 &&
+                         nd * 4 <= 4ll * ctx->N * ctx->N * (ctx->fp64 ? 8 : 4);
     }
     const long long gpb = ctx->block / ctx->L;
     const long long need = (ctx->B + gpb - 1) / gpb;

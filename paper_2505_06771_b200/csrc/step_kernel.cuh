@@ -637,6 +637,13 @@ __host__ __device__ constexpr bool qp_fast_first_row(int L) {
     return L == 4;
 }
 
+// Host-buffer obs staged in the group's QP workspace (StepParams::obs_ws_stage): compiled only into
+// the tasks whose warp stage costs too much (capi.cu's rule picks it for arctic_transport and
+// rware); in the others the extra branch alone cost 2-3 % (navigation, MT; profiles/r02/ab_ws_regress.log).
+__host__ __device__ constexpr bool obs_ws_stage_task(int task) {
+    return task == MRSIM_TASK_ARCTIC_TRANSPORT || task == MRSIM_TASK_RWARE;
+}
+
 // MULTI: the mrsim_rollout instantiation (p.n_steps steps per task); the single-step instantiation
 // compiles the step loop away (the loop and the input-copy select cost 2-6 % when always present).
 template <class Real, int L, int MP, int MO, int TASK, bool MULTI = false>
@@ -957,7 +964,7 @@ __device__ __forceinline__ void step_body(const StepParams<Real>& p) {
                     for (int k = threadIdx.x & 31; k < total; k += 32) dst[k] = wst[k];
                 }
                 __syncwarp();
-            } else if (obs_s && p.obs_ws_stage) {
+            } else if (obs_ws_stage_task(TASK) && obs_s && p.obs_ws_stage) {
                 // host-buffer steps whose warp stage would cost a resident block: each group stages
                 // its env's obs in its own QP inverse-Gram matrix (dead after the ticks), and the warp
                 // stores its consecutive envs' block as 8-byte pieces (256 contiguous bytes per store)
