@@ -427,7 +427,9 @@ __device__ __forceinline__ int barrier_filter(const Grp<L>& g, BarrierRows<Real,
         const Real dist2 = dx * dx + dy * dy;
         if (s < rows.npair && dist2 < Real(1e-18)) coincident = true;
         const Real h = dist2 - k.r_eff2;
-        const Real inv = rsqrt(Real(8) * dist2);
+        // empty slots (s >= npair: i = j = 0, dist2 = 0) take 1 so rsqrt stays on its fast path
+        // (rsqrt(0) calls the slow path: half a warp per tick at N = 4); their rows are never read
+        const Real inv = rsqrt(Real(8) * (s < rows.npair ? dist2 : Real(1)));
         rows.F(3 * s, lane) = Real(2) * dx * inv;
         rows.F(3 * s + 1, lane) = Real(2) * dy * inv;
         rows.F(3 * s + 2, lane) = k.gamma * h * h * h * inv;
