@@ -220,13 +220,11 @@ struct BarrierRows {
         F(kU + 1, lane) = uy;
         Grp<L>::sync();
 #pragma unroll
-        for (int s = 0; s < MP; ++s) {
-            if (s < npair && off(s)) {
-                const Real uxi = F(kU, pi[s]), uyi = F(kU + 1, pi[s]);
-                const Real uxj = F(kU, pj[s]), uyj = F(kU + 1, pj[s]);
-                consider(F(3 * s, lane) * (uxj - uxi) + F(3 * s + 1, lane) * (uyj - uyi) - F(3 * s + 2, lane),
-                         lane + s * L, worst, p);
-            }
+        for (int s = 0; s < MP; ++s) {  // branch-free: empty / active slots get -inf (their rows are finite)
+            const Real uxi = F(kU, pi[s]), uyi = F(kU + 1, pi[s]);
+            const Real uxj = F(kU, pj[s]), uyj = F(kU + 1, pj[s]);
+            const Real v = F(3 * s, lane) * (uxj - uxi) + F(3 * s + 1, lane) * (uyj - uyi) - F(3 * s + 2, lane);
+            consider((s < npair && off(s)) ? v : -Consts<Real>::inf, lane + s * L, worst, p);
         }
         if (valid) {
             const int w0 = P + 4 * lane;
@@ -874,7 +872,7 @@ __device__ __forceinline__ void step_body(const StepParams<Real>& p) {
                         const Real xi = rows.F(kU, rows.pi[s]), yi = rows.F(kU + 1, rows.pi[s]);
                         const Real xj = rows.F(kU, rows.pj[s]), yj = rows.F(kU + 1, rows.pj[s]);
                         const Real dx = xi - xj, dy = yi - yj;
-                        if (s < rows.npair) md2 = dmin(md2, dx * dx + dy * dy);
+                        md2 = dmin(md2, s < rows.npair ? dx * dx + dy * dy : Consts<Real>::inf);
                     }
                     md2 = g.min(md2);
                     min_d2 = dmin(min_d2, md2);
