@@ -62,7 +62,7 @@ struct Grp {
         for (int o = L / 2; o > 0; o >>= 1) {
             const T ov = __shfl_xor_sync(kFull, v, o, L);
             const int oi = __shfl_xor_sync(kFull, idx, o, L);
-            const bool take = ov > v || (ov == v && oi < idx);
+            const bool take = (ov > v) | ((ov == v) & (oi < idx));  // no short-circuit: no branch
             v = take ? ov : v;
             idx = take ? oi : idx;
         }
@@ -76,7 +76,7 @@ struct Grp {
         for (int o = L / 2; o > 0; o >>= 1) {
             const T ov = __shfl_xor_sync(kFull, v, o, L);
             const int oi = __shfl_xor_sync(kFull, idx, o, L);
-            const bool take = ov < v || (ov == v && oi < idx);
+            const bool take = (ov < v) | ((ov == v) & (oi < idx));
             v = take ? ov : v;
             idx = take ? oi : idx;
         }
